@@ -1,0 +1,20 @@
+"""fp64 CPU oracle for the VI-informed subset HMC hot path (arXiv 2507.14652).
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s
+`cpu_baseline` leg / `--impl reference` arm may import, call or execute anything under
+`oracle/`.  The product path (`paper_2507_14652_b200/`) never imports it and shares no
+code with it (no kernels, helpers, constants or table generators); the only common
+dependency is the seeded input generator package `hmcdata/`, which holds none of the
+method's arithmetic.
+
+Plain, slow, obviously-correct NumPy float64 implementation of:
+  network.py  - parameter layout, forward (MLP / DeepONet) and hand-written reverse mode
+  philox.py   - Philox4x32-10 counter RNG, uniforms and Box-Muller normals
+  hmc.py      - reduced-space log-posterior + gradient (Algorithm 2 target), momentum
+                draw, kick-drift-kick leapfrog, Metropolis-Hastings step, chains
+
+Each function cites the PAPER.md passage (P:line) or SURVEY.md reading it follows.
+Parity status: every function is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
+(closed forms, finite differences, invariants, known answers); see DESIGN.md §4.
+"""
+from . import network, philox, hmc  # noqa: F401

@@ -1,0 +1,206 @@
+"""Networks F_Theta in fp64: layout, forward, reverse mode.  TEST INFRASTRUCTURE ONLY
+(see oracle/__init__.py).
+
+PAPER.md P:68 (F_Theta parameterised by Theta in R^{N_Theta}), P:273 / P:335 (MLPs with
+sin / tanh), P:369 + P:527-539 (DeepONet: branch and trunk are feed-forward nets).
+DeepONet output F(u, y) = sum_k B_k(u) T_k(y) + b0.
+Flat layout: per net, per layer W[out x in] row-major then b[out];
+DeepONet b0 last.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def layer_table(arch):
+    """[(net, layer, w_off, b_off or None, n_out, n_in, act)] in flat order; plus b0 offset."""
+    rows = []
+    off = 0
+    for ni, net in enumerate(arch.nets):
+        for l in range(len(net.widths) - 1):
+            n_in, n_out = net.widths[l], net.widths[l + 1]
+            w_off = off
+            off += n_out * n_in
+            b_off = None
+            if net.bias[l]:
+                b_off = off
+                off += n_out
+            rows.append((ni, l, w_off, b_off, n_out, n_in, net.acts[l]))
+    b0 = None
+    if arch.has_b0:
+        b0 = off
+        off += 1
+    return rows, b0, off
+
+
+def param_count(arch) -> int:
+    return layer_table(arch)[2]
+
+
+def _act(name, z):
+    if name == "tanh":
+        return np.tanh(z)
+    if name == "sin":
+        return np.sin(z)
+    return z
+
+
+def _dact(name, z):
+    """d act / dz evaluated at the pre-activation z."""
+    if name == "tanh":
+        t = np.tanh(z)
+        return 1.0 - t * t
+    if name == "sin":
+        return np.cos(z)
+    return np.ones_like(z)
+
+
+def net_forward(arch, theta_full, ni, x):
+    """h_0 = x; z_l = h_{l-1} W_l^T + b_l; h_l = act_l(z_l), batched over rows of x.
+    Returns (output, [(h_in, z)] per layer) in fp64."""
+    rows, _, _ = layer_table(arch)
+    h = np.asarray(x, dtype=np.float64)
+    tape = []
+    for (n_idx, l, w_off, b_off, n_out, n_in, act) in rows:
+        if n_idx != ni:
+            continue
+        W = theta_full[w_off:w_off + n_out * n_in].reshape(n_out, n_in)
+        z = h @ W.T
+        if b_off is not None:
+            z = z + theta_full[b_off:b_off + n_out][None, :]
+        tape.append((h, z))
+        h = _act(act, z)
+    return h, tape
+
+
+def net_backward(arch, theta_full, ni, tape, dout, grad_full):
+    """Reverse mode through net ni given dL/d(output) = dout (rows x n_out).
+    Accumulates dL/dW_l = delta_l^T h_{l-1}, dL/db_l = sum_rows delta_l into grad_full."""
+    rows, _, _ = layer_table(arch)
+    mine = [r for r in rows if r[0] == ni]
+    g = np.asarray(dout, dtype=np.float64)
+    for li in range(len(mine) - 1, -1, -1):
+        (_, l, w_off, b_off, n_out, n_in, act) = mine[li]
+        h_in, z = tape[li]
+        delta = g * _dact(act, z)
+        grad_full[w_off:w_off + n_out * n_in] += (delta.T @ h_in).reshape(-1)
+        if b_off is not None:
+            grad_full[b_off:b_off + n_out] += delta.sum(axis=0)
+        W = theta_full[w_off:w_off + n_out * n_in].reshape(n_out, n_in)
+        g = delta @ W
+    return g
+
+
+def predict(arch, theta_full, data):
+    """F for every datum: MLP -> [n]; DeepONet -> [n_c, n_x] (each pair (c, x) is
+    F(u_c, y_x) = B(u_c) . T(y_x) + b0: branch evaluated once per function, trunk once
+    per query point, as the definition reads)."""
+    theta_full = np.asarray(theta_full, dtype=np.float64)
+    if arch.kind == "mlp":
+        out, _ = net_forward(arch, theta_full, 0, data["x"])
+        return out[:, 0]
+    B, _ = net_forward(arch, theta_full, 0, data["u"])
+    T, _ = net_forward(arch, theta_full, 1, data["q"])
+    _, b0, _ = layer_table(arch)
+    F = B @ T.T
+    if b0 is not None:
+        F = F + theta_full[b0]
+    return F
+
+
+def predict_pairwise(arch, theta_full, u_rows, q_rows):
+    """DeepONet evaluated pair by pair, F = sum_k B_k(u) T_k(y) + b0 - used by the
+    factored == pairwise pin."""
+    theta_full = np.asarray(theta_full, dtype=np.float64)
+    _, b0, _ = layer_table(arch)
+    out = np.empty(len(u_rows))
+    for i, (u, q) in enumerate(zip(u_rows, q_rows)):
+        B, _ = net_forward(arch, theta_full, 0, np.asarray(u)[None, :])
+        T, _ = net_forward(arch, theta_full, 1, np.asarray(q)[None, :])
+        s = 0.0
+        for kk in range(B.shape[1]):
+            s += B[0, kk] * T[0, kk]
+        out[i] = s + (theta_full[b0] if b0 is not None else 0.0)
+    return out
+
+
+def loglik_grad(arch, theta_full, data, sigma):
+    """Gaussian log-likelihood -sum (y - F)^2 / (2 sigma^2) (Table 5; constants
+    dropped, Q7) and its gradient over ALL flat parameters (fp64)."""
+    theta_full = np.asarray(theta_full, dtype=np.float64)
+    s2 = float(sigma) ** 2
+    grad = np.zeros_like(theta_full)
+    if arch.kind == "mlp":
+        F, tape = net_forward(arch, theta_full, 0, data["x"])
+        r = np.asarray(data["y"], dtype=np.float64) - F[:, 0]
+        ll = -np.dot(r, r) / (2.0 * s2)
+        net_backward(arch, theta_full, 0, tape, (r / s2)[:, None], grad)
+        return ll, grad, r
+    B, tb = net_forward(arch, theta_full, 0, data["u"])
+    T, tt = net_forward(arch, theta_full, 1, data["q"])
+    _, b0, _ = layer_table(arch)
+    F = B @ T.T
+    if b0 is not None:
+        F = F + theta_full[b0]
+    R = np.asarray(data["v"], dtype=np.float64) - F
+    ll = -np.sum(R * R) / (2.0 * s2)
+    E = R / s2                       # d ll / d F
+    net_backward(arch, theta_full, 0, tb, E @ T, grad)     # dF/dB_ck = T_xk
+    net_backward(arch, theta_full, 1, tt, E.T @ B, grad)   # dF/dT_xk = B_ck
+    if b0 is not None:
+        grad[b0] += E.sum()
+    return ll, grad, R
+
+
+def grad_abs_scale(arch, theta_full, data, sigma):
+    """Summation scale for element-wise gradient tolerances:
+    the same reverse mode run on absolute values, seeded with (|F| + |y|)/sigma^2, so
+    S_i >= sum over all product terms of |term| in d ll / d theta_i (the quantity a
+    floating-point error bound of the gradient is proportional to)."""
+    th = np.abs(np.asarray(theta_full, dtype=np.float64))
+    rows, b0, _ = layer_table(arch)
+    s2 = float(sigma) ** 2
+    S = np.zeros_like(th)
+
+    def fwd(ni, x):
+        h = np.asarray(x, dtype=np.float64)
+        hs, tape = [], []
+        th_signed = np.asarray(theta_full, dtype=np.float64)
+        for (n_idx, l, w_off, b_off, n_out, n_in, act) in rows:
+            if n_idx != ni:
+                continue
+            W = th_signed[w_off:w_off + n_out * n_in].reshape(n_out, n_in)
+            z = h @ W.T
+            if b_off is not None:
+                z = z + th_signed[b_off:b_off + n_out][None, :]
+            tape.append((h, z))
+            h = _act(act, z)
+        return h, tape
+
+    def bwd(ni, tape, dout):
+        mine = [r for r in rows if r[0] == ni]
+        g = dout
+        for li in range(len(mine) - 1, -1, -1):
+            (_, l, w_off, b_off, n_out, n_in, act) = mine[li]
+            h_in, z = tape[li]
+            delta = g * np.abs(_dact(act, z))
+            S[w_off:w_off + n_out * n_in] += (delta.T @ np.abs(h_in)).reshape(-1)
+            if b_off is not None:
+                S[b_off:b_off + n_out] += delta.sum(axis=0)
+            W = th[w_off:w_off + n_out * n_in].reshape(n_out, n_in)
+            g = delta @ W
+
+    if arch.kind == "mlp":
+        F, tape = fwd(0, data["x"])
+        seed = (np.abs(F[:, 0]) + np.abs(np.asarray(data["y"], dtype=np.float64))) / s2
+        bwd(0, tape, seed[:, None])
+        return S
+    B, tb = fwd(0, data["u"])
+    T, tt = fwd(1, data["q"])
+    F = B @ T.T + (np.asarray(theta_full, dtype=np.float64)[b0] if b0 is not None else 0.0)
+    E = (np.abs(F) + np.abs(np.asarray(data["v"], dtype=np.float64))) / s2
+    bwd(0, tb, E @ np.abs(T))
+    bwd(1, tt, E.T @ np.abs(B))
+    if b0 is not None:
+        S[b0] += E.sum()
+    return S
