@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Throughput of the VI-HMC hot path (full-batch leapfrog trajectory) on B200.
+
+metric (BASELINE.json): full-batch masked-gradient evals/sec and HMC samples/sec at 1/2/4/8 B200.
+A "step" = one HMC iteration (Algorithm 2) of every chain: L leapfrog steps, each a
+full-batch forward + backward over the whole training set, then the Metropolis test.
+value = chain gradient evaluations per second summed over all GPUs (C x L x K x N / t_max).
+
+Default workload: cfg5 (cone-surface DeepONet, 528,641 params, 20,000 active, 512 x 2048 pairs,
+64 chains, L = 200) - the north-star target config; `--cfg` selects another.
+N > 1 (torchrun): chain-parallel, C chains per GPU with global chain ids, no data-path collective
+("scaling": "weak").  `--impl reference` times the fp64 CPU oracle (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+WORKLOAD_DESC = {
+    "cfg1": "cfg1 tiny Bayesian MLP 1-20-20-1 tanh, 481 params all active, N=64",
+    "cfg2": "cfg2 MLP 1-64x4-1 tanh, 12,673 params, 1,267 active, N=1024",
+    "cfg3": "cfg3 MLP 8-256x3-1 tanh, 134,145 params, 6,707 active, N=16384",
+    "cfg4": "cfg4 DeepONet branch 100-128-128-128-100 / trunk 1-128-128-100, 88,521 params, 8,852 active, 1000x100 pairs",
+    "cfg5": "cfg5 cone-surface DeepONet branch 5-256x5 / trunk 2-256x5, 528,641 params, 20,000 active, 512x2048 pairs",
+}
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_FILE)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------------------ clocks ---
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except Exception:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------- CPU oracle ---
+def cpu_oracle_rate(prob, budget_s=12.0, min_evals=3):
+    """fp64 oracle full-batch gradient evaluations / s on this host (chain 0, initial state)."""
+    from oracle import hmc as ohmc
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = None
+    t = ohmc.Target(prob)
+    th = prob.frozen[prob.idx].astype(np.float64)
+    t.logp_grad(th)   # warm
+    n, t0 = 0, time.perf_counter()
+    while n < min_evals or time.perf_counter() - t0 < budget_s:
+        t.logp_grad(th)
+        n += 1
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    return n / dt, n, dt, cores, threads
+
+
+def run_reference(args):
+    """Reference arm: the fp64 oracle as it stands, one bounded sample per step (one oracle
+    trajectory of chain 0 truncated to --ref-L leapfrog steps)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from hmcdata import make_problem
+    from oracle import hmc as ohmc
+    prob = make_problem(args.cfg)
+    t = ohmc.Target(prob)
+    th = prob.frozen[prob.idx].astype(np.float64)
+    lp, g = t.logp_grad(th)
+    Lr = args.ref_L
+    for w in range(args.warmup):
+        r = ohmc.trajectory(t, th, lp, g, prob.eps, Lr, w, 0)
+        th, lp, g = r["theta"], r["logp"], r["grad"]
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        r = ohmc.trajectory(t, th, lp, g, prob.eps, Lr, args.warmup + s, 0)
+        th, lp, g = r["theta"], r["logp"], r["grad"]
+    dt = time.perf_counter() - t0
+    evals = Lr * args.steps
+    cores = len(os.sched_getaffinity(0))
+    value = evals / dt
+    out = {"impl": "reference", "metric": "full-batch masked-gradient evals/sec", "value": value,
+           "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
+           "config": {"workload": WORKLOAD_DESC[args.cfg], "chains": 1, "L_per_step": Lr},
+           "samples_per_s": args.steps / dt,
+           "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{args.steps} oracle trajectories of chain 0, each {Lr} leapfrog "
+                                      f"steps ({evals} full-batch fp64 gradient evaluations)"},
+           "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ----------------------------------------------------------------------------- our arm ---
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from hmcdata import make_problem
+    from paper_2507_14652_b200 import abi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    prob = make_problem(args.cfg)
+    C, k, L, eps = prob.n_chains, prob.k, prob.L, prob.eps
+    if args.L:
+        L = args.L
+    if args.eps:
+        eps = args.eps
+    ids = (rank * C + np.arange(C)).astype(np.uint32)
+    ctx = abi.Context(prob, mode="chain" if world > 1 else "single", rank=rank, world=world, chain_ids=ids)
+
+    th0 = np.repeat(prob.frozen[prob.idx][None, :], C, axis=0).astype(np.float32)  # Q20: start at mu_s
+    T = torch.as_tensor(th0, device=dev).contiguous()
+    LP = torch.empty(C, dtype=torch.float64, device=dev)
+    G = torch.empty(C, k, dtype=torch.float32, device=dev)
+    abi.hmc_grad(ctx.ctx, T, LP, G)
+    K, W = args.steps, args.warmup
+    smp = torch.empty(C, max(K, 1), k, dtype=torch.float32, device=dev)
+    acc = torch.empty(C, max(K, 1), dtype=torch.uint8, device=dev)
+    dH = torch.empty(C, max(K, 1), dtype=torch.float64, device=dev)
+    abi.hmc_profile(ctx.ctx, True)
+    it = 0
+    for _ in range(W):
+        abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, 1, smp, acc, dH)
+        it += 1
+    torch.cuda.synchronize()
+    gpu_index = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        gpu_index = vis.split(",")[local]
+    clk = Clocks(gpu_index)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, K, smp, acc, dH)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    it += K
+    t = e0.elapsed_time(e1) / 1000.0
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.item()
+    evals = world * C * L * K
+    value = evals / t
+    acc_rate = acc[:, :K].float().mean().item()
+
+    # ---- live per-kernel timing of the last timed trajectory (event nodes in the graph) ----
+    prof = abi.hmc_profile_read(ctx.ctx)
+    abi.hmc_profile(ctx.ctx, False)
+    per_class = {}
+    body_ms = [r[1] for r in prof if r[0] == "body" and r[1] > 0]
+    body_flops = next((r[2] for r in prof if r[0] == "body"), 0.0)
+    for name, ms, fl, by, step in prof:
+        if step == 0 and name not in ("body",):
+            d = per_class.setdefault(name, [0.0, 0.0, 0.0, 0])
+            d[0] += ms; d[1] += fl; d[2] += by; d[3] += 1
+    step0_total = sum(v[0] for v in per_class.values())
+    dom = max(per_class.items(), key=lambda kv: kv[1][0]) if per_class else None
+    peaks, peak_src = load_peaks()
+    engine = abi.hmc_engine_info(ctx.ctx)
+    roofline = None
+    if dom:
+        name, (ms, fl, by, nl) = dom
+        achieved = fl / (ms / 1000.0) / 1e12
+        if name.startswith("tc_"):
+            peak = peaks.get("bf16_tflops_sustained", 1393.9) * 0.5 / 3.0
+            bound, unit = "tensor", "TFLOP/s"
+            peak_note = (f"FP32-equivalent 3xTF32 peak = {peak_src} bf16 sustained x 0.5 (TF32/BF16 "
+                         f"nominal ratio) / 3")
+        else:
+            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+            bound, unit = "alu", "TFLOP/s"
+            peak_note = "SIMT FP32 FMA peak = 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md §5)"
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(args.cfg, {}).get(name)
+            except Exception:
+                traffic = None
+        roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                    "frac": achieved / peak, "traffic": traffic, "kernel": name,
+                    "launches_per_eval": nl, "ms_per_eval": ms,
+                    "share_of_step0": ms / step0_total if step0_total else None,
+                    "algorithmic_flops_per_eval": fl, "peak_source": peak_note}
+
+    # ---- e2e: same metric through the C-ABI with pinned host buffers (H2D/D2H inside) ----
+    e2e = None
+    if not args.no_e2e:
+        hT = T.cpu().pin_memory()
+        hLP = LP.cpu().pin_memory()
+        hG = G.cpu().pin_memory()
+        Ke = args.e2e_steps or K
+        hS = torch.empty(C, 1, k, dtype=torch.float32).pin_memory()
+        hA = torch.empty(C, 1, dtype=torch.uint8).pin_memory()
+        hD = torch.empty(C, 1, dtype=torch.float64).pin_memory()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(Ke):
+            abi.hmc_sample(ctx.ctx, hT, hLP, hG, eps, L, it + s, 1, hS, hA, hD)
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = tt.item()
+        h2d = C * k * 4 * 2 + C * 8
+        d2h = h2d + C * k * 4 + C + C * 8
+        e2e = {"value": world * C * L * Ke / te, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": Ke}
+
+    per_grad, base, per_step = abi.hmc_launch_counts(ctx.ctx)
+    launches = K * (base + L * per_step)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, n, dt, cores, threads = cpu_oracle_rate(prob, budget_s=args.cpu_budget)
+        cpu = {"value": rate, "unit": "evals/s", "cores": cores, "kind": "oracle",
+               "blas_threads": threads,
+               "sample": f"{n} full-batch fp64 gradient evaluations of chain 0 at the initial state "
+                         f"({dt:.1f} s, NumPy/OpenBLAS oracle as it stands)"}
+    mode = "chain-parallel" if world > 1 else "single"
+    out = {"metric": "full-batch masked-gradient evals/sec", "value": value, "unit": "evals/s",
+           "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": 1000 * t / K,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded generators of SURVEY §8(d); random-init frozen means)",
+           "config": {"workload": WORKLOAD_DESC[args.cfg], "chains_per_gpu": C, "L": L, "eps": eps,
+                      "P": prob.P, "k": k, "parallelism": f"{mode} x{world}", "engine": engine,
+                      "step": "one HMC iteration (L leapfrog steps + MH) of every chain",
+                      "eps_note": "configured eps; cfg4/cfg5 eps exceed the leapfrog stability limit "
+                                  "at the seeded state (DESIGN.md §3), proposals diverge and are "
+                                  "rejected; work per step is fixed by L",
+                      "l2": "inputs larger than L2: per-step working set (activations of all chains) "
+                            "exceeds the 126 MB L2, no flush needed"},
+           "samples_per_s": world * C * K / t, "acceptance": acc_rate,
+           "eval_ms_mean": (statistics.mean(body_ms) if body_ms else None),
+           "body_flops_per_eval_all_chains": body_flops,
+           "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+           "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(out))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--cfg", default="cfg5", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=0, help="override the config's leapfrog steps")
+    ap.add_argument("--eps", type=float, default=0.0, help="override the config's step size")
+    ap.add_argument("--ref-L", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: the contract needs >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

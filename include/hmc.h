@@ -1,0 +1,188 @@
+/*
+ * hmc.h - C ABI of libhmc.so: the full-batch leapfrog hot path of VI-informed subset HMC
+ * (Thiagarajan, Zaki, Shields, arXiv 2507.14652), built for NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n (LaTeX source of the paper); S:n = SPEC.md line n;
+ * "Qn" = the readings of ambiguous passages listed in DESIGN.md §3.
+ *
+ * The operation (Algorithm 2): the parameters Theta of a network F_Theta are split
+ * into an active subset Theta_s (k entries, flat indices idx) and a frozen subset Theta_~s fixed
+ * at the VI means mu_~s.  HMC samples the conditional posterior
+ * P(Theta_s | D, mu_~s) with Gaussian likelihood and a zero-mean Gaussian prior on
+ * Theta_s (Table 5):
+ *     log pi(theta_s) = -sum_n (y_n - F_n)^2 / (2 sigma^2) - sum_{i in s} theta_i^2 / (2 sigma_p^2)
+ * (normalising constants dropped, Q7; hmc_logpost_const returns them).  Each HMC iteration draws
+ * p ~ N(0, M), integrates Hamilton's equations with leapfrog (kick-drift-kick,
+ * Q2), and applies the Metropolis test r > u (accept iff ln u < H0 - H*, strict,
+ * non-finite rejects; Q4/Q5) with H = -log pi + 1/2 p^T M^-1 p (Q1), M diagonal (Q6).
+ *
+ * Conventions for every call:
+ *  - All functions return an int status: HMC_OK (0) or one of HMC_E_* below.  A failing call
+ *    leaves a message retrievable with hmc_last_error(ctx) (or hmc_last_error(NULL) for
+ *    failures before a context exists).  Non-finite log pi or H is NOT an error: it is
+ *    returned in the outputs and makes the proposal rejected.
+ *  - Pointers may be host or device memory (detected per pointer with cudaPointerGetAttributes);
+ *    host buffers are staged through pinned memory and the call synchronises the stream before
+ *    returning.  With device pointers the call is asynchronous on `stream`.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Flat parameter layout: per net, per linear layer W[out x in] row-major
+ *    then b[out] (if the layer has a bias); for a DeepONet branch layers, trunk layers, then
+ *    the scalar b0.  k-vectors are ordered by ascending flat index (idx order).
+ *  - Chain-batched arrays are chain-major: theta[C x k], samples[C x S x k].
+ *  - A context is bound to one CUDA device and is not thread-safe.
+ */
+#ifndef HMC_B200_H
+#define HMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------- */
+#define HMC_OK 0
+#define HMC_E_CONFIG 1 /* bad shape, mask, sigma, argument or unsupported arch */
+#define HMC_E_CUDA 3   /* a CUDA runtime / launch error */
+#define HMC_E_NCCL 4   /* an NCCL error (data mode) */
+#define HMC_E_OOM 5    /* device or pinned allocation failed */
+#define HMC_E_STATE 6  /* call out of order (e.g. NULL context) */
+
+/* ---- architecture ------------------------------------------------------------------------ */
+enum { HMC_MLP = 0, HMC_DEEPONET = 1 };
+enum { HMC_ACT_IDENTITY = 0, HMC_ACT_TANH = 1, HMC_ACT_SIN = 2 };
+enum { HMC_MODE_SINGLE = 0, HMC_MODE_DATA = 1, HMC_MODE_CHAIN = 2 };
+
+/* A feed-forward net with n_layers linear layers: widths[0] inputs ... widths[n_layers]
+ * outputs; layer l applies act[l] to (W_l h + b_l).  Arrays are host memory, read at setup. */
+typedef struct {
+  int32_t n_layers;
+  const int32_t* widths;   /* [n_layers + 1] */
+  const int32_t* acts;     /* [n_layers] HMC_ACT_* */
+  const int32_t* has_bias; /* [n_layers] 0/1 */
+} hmc_net;
+
+/* MLP: net[0] (output width must be 1).  DeepONet (Q14): net[0] = branch, net[1] = trunk,
+ * equal output widths p; F(u, y) = sum_k B_k(u) T_k(y) + b0 (b0 present iff has_b0). */
+typedef struct {
+  int32_t kind;
+  hmc_net net[2];
+  int32_t has_b0;
+} hmc_arch;
+
+/* Training data D, fp32 row-major, host or device; copied in at setup, the caller may
+ * free it on return.  MLP: x[n x d_in], y[n].  DeepONet (cartesian product layout, Q16):
+ * u[n_c x m] branch inputs (function samples at the sensors), q[n_x x d_t] trunk inputs,
+ * v[n_c x n_x] targets, pair (c, x) -> v[c * n_x + x].  In data mode these are this rank's
+ * shard (a row block of x/y, or of u/v for a DeepONet); n_global is the sum over ranks. */
+typedef struct {
+  const float* x;
+  const float* y;
+  int64_t n;
+  const float* u;
+  const float* q;
+  const float* v;
+  int64_t n_c, n_x;
+  int64_t n_global;
+} hmc_data;
+
+typedef struct {
+  const float* frozen;  /* [P] full flat mu; entries at idx are ignored (the state sets them) */
+  const int32_t* idx;   /* [k] strictly ascending active flat indices, 1 <= k <= P */
+  int64_t P, k;
+  double noise_sigma;   /* likelihood sd sigma > 0 (Table 5 lists sigma^2, Q9) */
+  double prior_sigma;   /* prior sd sigma_p > 0 on every active entry (Q8, Q10) */
+  const float* inv_mass; /* [k] diagonal M^-1 (> 0) or NULL for identity (Q6) */
+  uint64_t seed;        /* Philox key (Q23) */
+  int32_t n_chains;     /* chains on this rank */
+  const uint32_t* chain_ids; /* [n_chains] global chain ids keying Philox, or NULL = 0..C-1 */
+  int32_t mode;         /* HMC_MODE_*; DATA needs world > 1 ranks sharing one chain set */
+  int32_t rank, world;  /* this rank, number of ranks (1 for SINGLE / CHAIN) */
+  const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode only) */
+} hmc_config;
+
+typedef struct hmc_ctx hmc_ctx;
+
+/* Rank 0 creates an NCCL unique id (128 bytes) to be broadcast to the other ranks. */
+int hmc_comm_unique_id(uint8_t id_out[128]);
+
+/* Validates arch/data/config (HMC_E_CONFIG with a message naming the field), uploads data,
+ * frozen values and the mask, allocates all device workspace for n_chains chains, and (DATA
+ * mode) creates the NCCL communicator.  Binds the context to the current CUDA device.
+ * On success *out owns everything; release with hmc_destroy. */
+int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, void* stream,
+              hmc_ctx** out);
+
+/* One full-batch gradient evaluation for every chain ("forward pass ... gradient
+ * computation"): logp[c] = log pi(theta[c]) (constants dropped) in fp64 and
+ * grad[c] = d log pi / d theta_s (ascent direction) in fp32.  theta [C x k] in, logp [C],
+ * grad [C x k] out.  In DATA mode every rank receives identical values. */
+int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream);
+
+/* The dropped constant: -N log(sigma sqrt(2 pi)) - k log(sigma_p sqrt(2 pi)) (N = n_global or
+ * n_c x n_x global), so logp + c is S:362's normalised value. */
+int hmc_logpost_const(const hmc_ctx* ctx, double* c);
+
+/* One Algorithm-2 iteration for every chain: momentum p ~ N(0, M) from Philox
+ * (seed, tag 0, iter, chain_id) (Q23 / DESIGN §3), L kick-drift-kick steps of size eps with the
+ * start gradient taken from `grad` (the cache), Metropolis test with u from Philox tag 1.
+ * theta[C x k], logp[C], grad[C x k] are in/out: on accept they become the proposal's, on
+ * reject they are unchanged.  acc[C] (0/1) and dH[C] = H* - H0 are outputs (either may be NULL).
+ * L = 0 is the identity and always accepts.  eps must be finite and > 0, L >= 0,
+ * 0 <= iter < 2^32. */
+int hmc_trajectory(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L,
+                   int64_t iter, uint8_t* acc, double* dH, void* stream);
+
+/* Exactly S consecutive hmc_trajectory iterations iter0 .. iter0+S-1, replayed as one CUDA graph
+ * per trajectory with no host round trip.  samples[C x S x k] (state after each iteration),
+ * acc[C x S], dH[C x S] are outputs (acc / dH may be NULL).  Burn-in and thinning are the
+ * caller's.  Resuming at iter0 + S with the returned state is bitwise identical to one call. */
+int hmc_sample(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L,
+               int64_t iter0, int32_t S, float* samples, uint8_t* acc, double* dH, void* stream);
+
+/* Frees every resource of the context (NULL is a no-op). */
+int hmc_destroy(hmc_ctx* ctx);
+
+/* Context-owned message of the last failure (thread-local global when ctx == NULL). */
+const char* hmc_last_error(const hmc_ctx* ctx);
+
+/* ---- diagnostics used by tests and bench.py ---------------------------------------------- */
+
+/* Counts of this library's kernel launches: per hmc_grad call, and per trajectory as
+ * base + L * per_step. */
+int hmc_launch_counts(const hmc_ctx* ctx, int64_t* per_grad, int64_t* per_traj_base,
+                      int64_t* per_step);
+
+/* Raw Philox4x32-10 words for counters (j, tag, iter, chain), j < nblocks, key from seed:
+ * out[4 * j + w] (device or host pointer).  Used for the bitwise RNG agreement test. */
+int hmc_philox_words(uint64_t seed, uint32_t tag, uint32_t iter, uint32_t chain, int64_t nblocks,
+                     uint32_t* out, void* stream);
+
+/* Momentum draw of `hmc_trajectory`: p[C x k] = sqrt(m) z for the given iter (fp32 out). */
+int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream);
+
+/* Name of the GEMM engine used for each layer GEMM class ("simt" or "tcgen05"). */
+const char* hmc_engine_info(const hmc_ctx* ctx);
+
+/* Live kernel timing.  hmc_profile(ctx, 1) makes the next trajectory graph capture CUDA event
+ * nodes (cudaEventRecordExternal) around every kernel of the FIRST leapfrog step and around the
+ * gradient-evaluation body of EVERY step; hmc_profile_read returns, for the most recently
+ * replayed trajectory, one record per bracketed launch: kernel name, duration (ms), algorithmic
+ * FLOPs and bytes of that launch, and the leapfrog step (-1 for begin / Metropolis).  Records
+ * named "body" cover a whole gradient evaluation of step `step`.  Synchronises the context. */
+typedef struct {
+  char name[64];
+  double ms;
+  double flops;
+  double bytes;
+  int32_t step;
+} hmc_prof_rec;
+int hmc_profile(hmc_ctx* ctx, int32_t enable);
+int hmc_profile_read(hmc_ctx* ctx, int32_t max_recs, hmc_prof_rec* out, int32_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMC_B200_H */

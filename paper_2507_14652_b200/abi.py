@@ -1,0 +1,283 @@
+"""Thin ctypes binding of libhmc.so (include/hmc.h).  Argument marshalling only: every step of
+the hot path runs in the library's CUDA kernels.  There is no CPU fallback - if the library is
+missing or fails to load, every call raises.
+
+Arrays may be torch tensors (device or host, contiguous, matching dtype) or NumPy arrays (host).
+The functions keep the C names: hmc_setup, hmc_grad, hmc_trajectory, hmc_sample, ...
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+HMC_OK, HMC_E_CONFIG, HMC_E_CUDA, HMC_E_NCCL, HMC_E_OOM, HMC_E_STATE = 0, 1, 3, 4, 5, 6
+HMC_MLP, HMC_DEEPONET = 0, 1
+ACT = {"identity": 0, "tanh": 1, "sin": 2}
+MODE = {"single": 0, "data": 1, "chain": 2}
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
+
+
+class HmcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libhmc status {code}: {msg}")
+        self.code = code
+
+
+class hmc_net(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("widths", ctypes.POINTER(ctypes.c_int32)),
+                ("acts", ctypes.POINTER(ctypes.c_int32)), ("has_bias", ctypes.POINTER(ctypes.c_int32))]
+
+
+class hmc_arch(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("net", hmc_net * 2), ("has_b0", ctypes.c_int32)]
+
+
+class hmc_data(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("n", ctypes.c_int64),
+                ("u", ctypes.c_void_p), ("q", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("n_c", ctypes.c_int64), ("n_x", ctypes.c_int64), ("n_global", ctypes.c_int64)]
+
+
+class hmc_config(ctypes.Structure):
+    _fields_ = [("frozen", ctypes.c_void_p), ("idx", ctypes.c_void_p), ("P", ctypes.c_int64),
+                ("k", ctypes.c_int64), ("noise_sigma", ctypes.c_double),
+                ("prior_sigma", ctypes.c_double), ("inv_mass", ctypes.c_void_p),
+                ("seed", ctypes.c_uint64), ("n_chains", ctypes.c_int32),
+                ("chain_ids", ctypes.c_void_p), ("mode", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+
+
+EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
+           "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
+           "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read"]
+
+
+class hmc_prof_rec(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 64), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
+                ("bytes", ctypes.c_double), ("step", ctypes.c_int32)]
+
+_lib = None
+
+
+def lib():
+    """Load libhmc.so (in-tree build).  Raises if it is missing: no fallback exists."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is not built; run `make` or __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u32, u64, dbl = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                   ctypes.c_uint64, ctypes.c_double)
+    L.hmc_comm_unique_id.argtypes = [vp]
+    L.hmc_setup.argtypes = [ctypes.POINTER(hmc_arch), ctypes.POINTER(hmc_data),
+                            ctypes.POINTER(hmc_config), vp, ctypes.POINTER(vp)]
+    L.hmc_grad.argtypes = [vp, vp, vp, vp, vp]
+    L.hmc_logpost_const.argtypes = [vp, ctypes.POINTER(dbl)]
+    L.hmc_trajectory.argtypes = [vp, vp, vp, vp, dbl, i32, i64, vp, vp, vp]
+    L.hmc_sample.argtypes = [vp, vp, vp, vp, dbl, i32, i64, i32, vp, vp, vp, vp]
+    L.hmc_destroy.argtypes = [vp]
+    L.hmc_last_error.argtypes = [vp]
+    L.hmc_last_error.restype = ctypes.c_char_p
+    L.hmc_launch_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.hmc_philox_words.argtypes = [u64, u32, u32, u32, i64, vp, vp]
+    L.hmc_momentum.argtypes = [vp, i64, vp, vp]
+    L.hmc_engine_info.argtypes = [vp]
+    L.hmc_engine_info.restype = ctypes.c_char_p
+    L.hmc_profile.argtypes = [vp, i32]
+    L.hmc_profile_read.argtypes = [vp, i32, ctypes.POINTER(hmc_prof_rec), ctypes.POINTER(i32)]
+    for name in EXPORTS:
+        if name not in ("hmc_last_error", "hmc_engine_info"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _ptr(a, keep: list, dtype=None):
+    """Raw pointer of a torch tensor or NumPy array (None -> NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):          # torch.Tensor
+        assert a.is_contiguous(), "tensors must be contiguous"
+        keep.append(a)
+        return a.data_ptr()
+    arr = np.ascontiguousarray(a, dtype=dtype) if dtype is not None else np.ascontiguousarray(a)
+    keep.append(arr)
+    return arr.ctypes.data
+
+
+def _check(rc, ctx=None):
+    if rc != HMC_OK:
+        msg = lib().hmc_last_error(ctx)
+        raise HmcError(rc, msg.decode() if msg else "")
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def hmc_comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().hmc_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def make_arch(kind: str, nets, has_b0: bool, keep: list) -> hmc_arch:
+    """nets: sequence of (widths, acts, has_bias) python sequences."""
+    a = hmc_arch()
+    a.kind = HMC_MLP if kind == "mlp" else HMC_DEEPONET
+    for i, (widths, acts, bias) in enumerate(nets):
+        w = (ctypes.c_int32 * len(widths))(*widths)
+        ac = (ctypes.c_int32 * len(acts))(*[ACT[x] if isinstance(x, str) else int(x) for x in acts])
+        b = (ctypes.c_int32 * len(bias))(*[int(bool(x)) for x in bias])
+        keep += [w, ac, b]
+        a.net[i] = hmc_net(len(widths) - 1, w, ac, b)
+    a.has_b0 = int(bool(has_b0))
+    return a
+
+
+def hmc_setup(arch: hmc_arch, data: hmc_data, cfg: hmc_config, stream=None) -> int:
+    ctx = ctypes.c_void_p()
+    _check(lib().hmc_setup(ctypes.byref(arch), ctypes.byref(data), ctypes.byref(cfg),
+                           _stream(stream), ctypes.byref(ctx)))
+    return ctx.value
+
+
+def hmc_grad(ctx, theta, logp, grad, stream=None):
+    keep = []
+    _check(lib().hmc_grad(ctx, _ptr(theta, keep, np.float32), _ptr(logp, keep),
+                          _ptr(grad, keep), _stream(stream)), ctx)
+
+
+def hmc_logpost_const(ctx) -> float:
+    c = ctypes.c_double()
+    _check(lib().hmc_logpost_const(ctx, ctypes.byref(c)), ctx)
+    return c.value
+
+
+def hmc_trajectory(ctx, theta, logp, grad, eps, L, it, acc=None, dH=None, stream=None):
+    keep = []
+    _check(lib().hmc_trajectory(ctx, _ptr(theta, keep), _ptr(logp, keep), _ptr(grad, keep),
+                                float(eps), int(L), int(it), _ptr(acc, keep), _ptr(dH, keep),
+                                _stream(stream)), ctx)
+
+
+def hmc_sample(ctx, theta, logp, grad, eps, L, iter0, S, samples, acc=None, dH=None, stream=None):
+    keep = []
+    _check(lib().hmc_sample(ctx, _ptr(theta, keep), _ptr(logp, keep), _ptr(grad, keep), float(eps),
+                            int(L), int(iter0), int(S), _ptr(samples, keep), _ptr(acc, keep),
+                            _ptr(dH, keep), _stream(stream)), ctx)
+
+
+def hmc_destroy(ctx):
+    if ctx:
+        _check(lib().hmc_destroy(ctx))
+
+
+def hmc_launch_counts(ctx):
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().hmc_launch_counts(ctx, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), ctx)
+    return a.value, b.value, c.value
+
+
+def hmc_philox_words(seed, tag, it, chain, nblocks, out, stream=None):
+    keep = []
+    _check(lib().hmc_philox_words(int(seed), int(tag), int(it), int(chain), int(nblocks),
+                                  _ptr(out, keep), _stream(stream)))
+
+
+def hmc_momentum(ctx, it, out, stream=None):
+    keep = []
+    _check(lib().hmc_momentum(ctx, int(it), _ptr(out, keep), _stream(stream)), ctx)
+
+
+def hmc_engine_info(ctx) -> str:
+    return lib().hmc_engine_info(ctx).decode()
+
+
+def hmc_profile(ctx, enable: bool):
+    _check(lib().hmc_profile(ctx, int(bool(enable))), ctx)
+
+
+def hmc_profile_read(ctx):
+    """[(name, ms, flops, bytes, step)] of the last replayed trajectory."""
+    n = ctypes.c_int32()
+    _check(lib().hmc_profile_read(ctx, 0, None, ctypes.byref(n)), ctx)
+    recs = (hmc_prof_rec * max(n.value, 1))()
+    _check(lib().hmc_profile_read(ctx, n.value, recs, ctypes.byref(n)), ctx)
+    return [(r.name.decode(), r.ms, r.flops, r.bytes, r.step) for r in recs[:n.value]]
+
+
+class Context:
+    """Owns one libhmc context built from a problem description (any object with the fields of
+    hmcdata.Problem: arch, x/y or u/q/v, frozen, idx, noise_sigma, prior_sigma, inv_mass, seed,
+    n_chains, chain_ids).  Marshalling only."""
+
+    def __init__(self, problem, mode: str = "single", rank: int = 0, world: int = 1,
+                 nccl_id: Optional[bytes] = None, n_global: int = 0, chain_ids=None,
+                 n_chains: Optional[int] = None):
+        keep = []
+        arch = problem.arch
+        nets = [(n.widths, n.acts, n.bias) for n in arch.nets]
+        a = make_arch(arch.kind, nets, arch.has_b0, keep)
+        d = hmc_data()
+        if arch.kind == "mlp":
+            d.x = _ptr(problem.x, keep, np.float32)
+            d.y = _ptr(problem.y, keep, np.float32)
+            d.n = int(problem.x.shape[0])
+        else:
+            d.u = _ptr(problem.u, keep, np.float32)
+            d.q = _ptr(problem.q, keep, np.float32)
+            d.v = _ptr(problem.v, keep, np.float32)
+            d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.q.shape[0])
+        d.n_global = int(n_global)
+        c = hmc_config()
+        c.frozen = _ptr(problem.frozen, keep, np.float32)
+        c.idx = _ptr(problem.idx, keep, np.int32)
+        c.P = int(problem.frozen.shape[0])
+        c.k = int(problem.idx.shape[0])
+        c.noise_sigma = float(problem.noise_sigma)
+        c.prior_sigma = float(problem.prior_sigma)
+        c.inv_mass = _ptr(problem.inv_mass, keep, np.float32) if problem.inv_mass is not None else None
+        c.seed = int(problem.seed)
+        C = int(n_chains if n_chains is not None else problem.n_chains)
+        c.n_chains = C
+        ids = chain_ids if chain_ids is not None else getattr(problem, "chain_ids", None)
+        if ids is not None:
+            ids = np.asarray(ids, dtype=np.uint32)[:C]
+            if ids.shape[0] < C:
+                ids = None
+        c.chain_ids = _ptr(ids, keep, np.uint32) if ids is not None else None
+        c.mode = MODE[mode]
+        c.rank, c.world = int(rank), int(world)
+        if nccl_id is not None:
+            idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
+            keep.append(idbuf)
+            c.nccl_id = ctypes.addressof(idbuf)
+        self.ctx = hmc_setup(a, d, c)
+        self.C, self.k, self.P = C, c.k, c.P
+
+    def close(self):
+        if self.ctx:
+            hmc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -1,0 +1,70 @@
+// Shared device helpers for libhmc (sm_100a).  Product code only: nothing here is shared
+// with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hmc {
+
+enum Act : int { ACT_ID = 0, ACT_TANH = 1, ACT_SIN = 2 };
+
+// Philox4x32-10 (counter-based RNG; DESIGN.md §3 "RNG").  Round function as in the
+// Random123 construction: two 32x32->64 multiplies, xor with the key, key bumped by the
+// Weyl constants between rounds.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    if (r < 9) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
+  return c;
+}
+
+// u = (x + 0.5) 2^-32 in fp64, strictly inside (0, 1).
+__device__ __forceinline__ double u01(uint32_t x) { return ((double)x + 0.5) * 2.3283064365386963e-10; }
+
+// Four standard normals from one Philox block by Box-Muller on (u0,u1) and (u2,u3), fp64.
+__device__ __forceinline__ void box_muller4(uint4 w, double z[4]) {
+  const double r01 = sqrt(-2.0 * log(u01(w.x)));
+  const double r23 = sqrt(-2.0 * log(u01(w.z)));
+  double s, c;
+  sincospi(2.0 * u01(w.y), &s, &c);
+  z[0] = r01 * c;
+  z[1] = r01 * s;
+  sincospi(2.0 * u01(w.w), &s, &c);
+  z[2] = r23 * c;
+  z[3] = r23 * s;
+}
+
+__device__ __forceinline__ float act_fwd(int act, float z) {
+  if (act == ACT_TANH) return tanhf(z);
+  if (act == ACT_SIN) return sinf(z);
+  return z;
+}
+
+// Deterministic block reduction of a double (fixed tree; every call site uses the same
+// blockDim so the summation order is a function of the data layout only).
+template <int NT>
+__device__ __forceinline__ double block_sum_d(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+}  // namespace hmc

@@ -1,0 +1,993 @@
+// libhmc: C-ABI implementation (include/hmc.h) of the VI-informed subset HMC hot path on B200.
+//
+// A gradient evaluation is a fixed sequence of kernels on the context's stream:
+//   scatter theta_s -> dense per-chain parameters
+//   forward  : layer GEMMs + fused bias/activation epilogue, output layer + residual^2 reduction
+//   backward : input-gradient GEMMs with fused act' epilogue, weight-gradient GEMMs restricted
+//              to the mask and compacted into the k-vector (P:257 last sentence)
+//   [DATA mode: NCCL all-reduce of the likelihood sums]
+//   finalize : prior, log pi in fp64, leapfrog kick/drift
+// A trajectory = momentum + L such steps + Metropolis, captured as ONE CUDA graph.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hmc.h"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+
+using namespace hmc;
+
+static thread_local std::string g_err;
+
+namespace {
+
+struct LayerInfo {
+  int net = 0, l = 0, n_in = 0, n_out = 0, act = 0;
+  bool bias = false, any_active = false;
+  int64_t w_off = 0, b_off = -1, rows = 0;
+  float* A = nullptr;  // [C x rows x n_out] layer output (hidden layers)
+  float* D = nullptr;  // [C x rows x n_out] cos(z) for sin layers
+};
+
+struct NetInfo {
+  std::vector<int> layers;  // indices into ctx->layers
+  int l_min = -1;           // lowest layer (position in `layers`) with an active parameter
+  int64_t rows = 0;
+  const float* input = nullptr;
+  int max_w = 0;
+  float* G[2] = {nullptr, nullptr};
+};
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+struct hmc_ctx {
+  int dev = 0, kind = 0, C = 0, mode = 0, rank = 0, world = 1;
+  int64_t P = 0, k = 0;
+  int64_t n = 0, n_c = 0, n_x = 0, n_global = 0, d_in = 0;
+  double sigma = 1, sigma_p = 1;
+  uint64_t seed = 0;
+  bool has_b0 = false;
+  int64_t b0_off = -1;
+  int b0_slot = -1;
+  std::vector<LayerInfo> layers;
+  NetInfo nets[2];
+  int n_nets = 1;
+  // device memory
+  DevBuf mem;
+  float *d_x = nullptr, *d_y = nullptr, *d_u = nullptr, *d_q = nullptr, *d_v = nullptr;
+  float* Wd = nullptr;
+  int32_t *d_idx = nullptr, *d_slot = nullptr;
+  float* d_inv_mass = nullptr;
+  uint32_t* d_chain = nullptr;
+  float *cur_theta = nullptr, *cur_grad = nullptr, *wrk_theta = nullptr, *wrk_grad = nullptr, *p = nullptr;
+  double *cur_logp = nullptr, *wrk_logp = nullptr, *H0 = nullptr;
+  float* gl = nullptr;
+  double* lik = nullptr;
+  double *part_sq = nullptr, *part_r = nullptr;
+  int n_part = 0;
+  float* R = nullptr;
+  float* colred = nullptr;
+  int colred_chunks = 0;
+  double* d_eps = nullptr;
+  Rec* d_rec = nullptr;
+  uint8_t* tmp_acc = nullptr;
+  double* tmp_dH = nullptr;
+  // pinned staging
+  Rec* h_rec = nullptr;
+  double* h_eps = nullptr;
+  cudaEvent_t ev_stage = nullptr, ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t st = nullptr;
+  // graphs
+  cudaGraphExec_t grad_exec = nullptr;
+  cudaGraphExec_t traj_exec = nullptr;
+  int traj_L = -1;
+  // comm
+  ncclComm_t comm = nullptr;
+  // live profiling (event nodes inside the trajectory graph)
+  struct ProfRec {
+    cudaEvent_t a = nullptr, b = nullptr;
+    std::string name;
+    double flops = 0, bytes = 0;
+    int step = -1;
+  };
+  std::vector<ProfRec> prof;
+  bool prof_on = false, prof_armed = false;
+  int prof_step = -1;
+  void prof_clear() {
+    for (auto& r : prof) {
+      if (r.a) cudaEventDestroy(r.a);
+      if (r.b) cudaEventDestroy(r.b);
+    }
+    prof.clear();
+  }
+  // bookkeeping
+  int64_t launches = 0;
+  int64_t per_body = 0;
+  double body_flops = 0, flop_acc = 0;
+  std::string err;
+  std::string engine;
+  TcPlanner tc;
+
+  KState kstate() const {
+    KState s;
+    s.C = C; s.k = k; s.P = P; s.idx = d_idx; s.inv_mass = d_inv_mass; s.chain_ids = d_chain;
+    s.Wd = Wd; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
+    s.wrk_theta = wrk_theta; s.wrk_grad = wrk_grad; s.wrk_logp = wrk_logp; s.p = p; s.H0 = H0;
+    s.gl = gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
+    s.eps = d_eps; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
+    return s;
+  }
+  ~hmc_ctx() {
+    prof_clear();
+    if (grad_exec) cudaGraphExecDestroy(grad_exec);
+    if (traj_exec) cudaGraphExecDestroy(traj_exec);
+    if (comm) ncclCommDestroy(comm);
+    if (h_rec) cudaFreeHost(h_rec);
+    if (h_eps) cudaFreeHost(h_eps);
+    if (ev_stage) cudaEventDestroy(ev_stage);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct Fail {
+  int code;
+};
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      err = std::string(#call) + ": " + cudaGetErrorString(e_);                               \
+      throw Fail{e_ == cudaErrorMemoryAllocation ? HMC_E_OOM : HMC_E_CUDA};                   \
+    }                                                                                         \
+  } while (0)
+
+#define CKN(call)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) {                                                                  \
+      err = std::string(#call) + ": " + ncclGetErrorString(r_);                               \
+      throw Fail{HMC_E_NCCL};                                                                 \
+    }                                                                                         \
+  } while (0)
+
+#define CFG(cond, msg)                                                                        \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      err = std::string("config: ") + (msg);                                                  \
+      throw Fail{HMC_E_CONFIG};                                                               \
+    }                                                                                         \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+T* dalloc(hmc_ctx* x, size_t count, std::string& err) {
+  void* p = nullptr;
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = 16;
+  CK(cudaMalloc(&p, bytes));
+  x->mem.ptrs.push_back(p);
+  CK(cudaMemset(p, 0, bytes));
+  return (T*)p;
+}
+
+// copy `count` elements of a host-or-device array to host
+template <typename T>
+std::vector<T> to_host(const T* src, size_t count, std::string& err) {
+  std::vector<T> h(count);
+  if (count) CK(cudaMemcpy(h.data(), src, count * sizeof(T), cudaMemcpyDefault));
+  return h;
+}
+
+int pick_bm(int M, int N) { return (M <= 64 || N <= 64) ? 64 : 128; }
+
+void launch_gemm_simt(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st) {
+  const int bm = pick_bm(a.M, a.N);
+  dim3 grid((a.N + bm - 1) / bm, (a.M + bm - 1) / bm, a.batch);
+#define GL(BM, AK, BK) gemm_simt_kernel<BM, AK, BK><<<grid, 256, 0, st>>>(a)
+  if (bm == 128) {
+    if (akm && bkm) GL(128, true, true);
+    else if (akm && !bkm) GL(128, true, false);
+    else if (!akm && !bkm) GL(128, false, false);
+    else GL(128, false, true);
+  } else {
+    if (akm && bkm) GL(64, true, true);
+    else if (akm && !bkm) GL(64, true, false);
+    else if (!akm && !bkm) GL(64, false, false);
+    else GL(64, false, true);
+  }
+#undef GL
+  x->launches++;
+}
+
+GemmArgs gemm_base(int M, int N, int K, int batch) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = M; a.N = N; a.K = K; a.batch = batch; a.ones_col = -1; a.epi = EPI_STORE;
+  return a;
+}
+
+// event pair around one launch while a profiled capture is armed (or always, for "body")
+int prof_begin(hmc_ctx* x, cudaStream_t st, bool force = false) {
+  if (!(x->prof_armed || (force && x->prof_on))) return -1;
+  hmc_ctx::ProfRec r;
+  r.step = x->prof_step;
+  if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return -1;
+  cudaEventRecordWithFlags(r.a, st, cudaEventRecordExternal);
+  x->prof.push_back(r);
+  return (int)x->prof.size() - 1;
+}
+
+void prof_end(hmc_ctx* x, int id, cudaStream_t st, const std::string& name, double flops, double bytes) {
+  if (id < 0) return;
+  auto& r = x->prof[id];
+  cudaEventRecordWithFlags(r.b, st, cudaEventRecordExternal);
+  r.name = name;
+  r.flops = flops;
+  r.bytes = bytes;
+}
+
+void launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag) {
+  const int id = prof_begin(x, st);
+  const bool tc = x->tc.accepts(a, akm, bkm);
+  if (tc) {
+    x->tc.launch(a, akm, bkm, st);
+    x->launches++;
+  } else {
+    launch_gemm_simt(x, a, akm, bkm, st);
+  }
+  const double flops = 2.0 * a.M * a.N * (double)a.K * a.batch;
+  const double bytes = 4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N);
+  x->flop_acc += flops;
+  prof_end(x, id, st, std::string(tc ? "tc_" : "simt_") + tag, flops, bytes);
+}
+
+inline const float* layer_input(hmc_ctx* x, const NetInfo& N, int i, int64_t* stride) {
+  if (i == 0) {
+    *stride = 0;
+    return N.input;
+  }
+  const LayerInfo& P = x->layers[N.layers[i - 1]];
+  *stride = P.rows * P.n_out;
+  return P.A;
+}
+
+void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
+  LayerInfo& L = x->layers[N.layers[i]];
+  int64_t s_in;
+  const float* in = layer_input(x, N, i, &s_in);
+  GemmArgs a = gemm_base((int)L.rows, L.n_out, L.n_in, x->C);
+  a.A = in; a.lda = L.n_in; a.sA = s_in;
+  a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
+  a.C = L.A; a.ldc = L.n_out; a.sC = L.rows * L.n_out;
+  a.epi = EPI_FWD; a.act = L.act;
+  if (L.bias) { a.bias = x->Wd + L.b_off; a.s_bias = x->P; }
+  if (L.act == ACT_SIN) { a.D = L.D; a.ldd = L.n_out; a.sD = L.rows * L.n_out; }
+  launch_gemm(x, a, true, true, st, "fwd");
+}
+
+// backward through layers i = top .. l_min of a net; G of layer `top` is in N.G[cur]
+void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t st) {
+  for (int i = top; i >= N.l_min; --i) {
+    LayerInfo& L = x->layers[N.layers[i]];
+    const float* G = N.G[cur];
+    int64_t s_in;
+    const float* in = layer_input(x, N, i, &s_in);
+    if (L.any_active) {
+      GemmArgs a = gemm_base(L.n_out, L.n_in + (L.bias ? 1 : 0), (int)L.rows, x->C);
+      a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
+      a.B = in; a.ldb = L.n_in; a.sB = s_in;
+      a.ones_col = L.bias ? L.n_in : -1;
+      a.epi = EPI_WGRAD;
+      a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
+      a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
+      launch_gemm(x, a, false, false, st, "wgrad");
+    }
+    if (i > N.l_min) {
+      const LayerInfo& Pv = x->layers[N.layers[i - 1]];
+      GemmArgs a = gemm_base((int)L.rows, L.n_in, L.n_out, x->C);
+      a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
+      a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
+      a.C = N.G[cur ^ 1]; a.ldc = L.n_in; a.sC = L.rows * L.n_in;
+      a.epi = EPI_DACT; a.act = Pv.act;
+      a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
+      launch_gemm(x, a, true, false, st, "dgrad");
+      cur ^= 1;
+    }
+  }
+}
+
+// forward + backward of one full-batch gradient evaluation (likelihood part only)
+void enqueue_body(hmc_ctx* x, cudaStream_t st) {
+  const int C = x->C;
+  if (x->kind == HMC_MLP) {
+    NetInfo& N = x->nets[0];
+    const int nl = (int)N.layers.size();
+    for (int i = 0; i < nl - 1; ++i) enqueue_forward_hidden(x, N, i, st);
+    LayerInfo& O = x->layers[N.layers[nl - 1]];
+    int64_t s_in;
+    const float* in = layer_input(x, N, nl - 1, &s_in);
+    {
+      const int id = prof_begin(x, st);
+      dim3 grid(x->n_part, C);
+      k_out_fwd<<<grid, 256, O.n_in * sizeof(float), st>>>(in, s_in, O.n_in, O.rows, x->Wd, x->P, O.w_off,
+                                                           O.b_off, x->d_y, x->R, 1.0 / (x->sigma * x->sigma),
+                                                           x->part_sq, x->n_part);
+      x->launches++;
+      x->flop_acc += 2.0 * C * O.rows * O.n_in;
+      prof_end(x, id, st, "out_fwd", 2.0 * C * O.rows * O.n_in, 4.0 * C * O.rows * (O.n_in + 1));
+    }
+    if (N.l_min < 0) return;
+    if (O.any_active) {
+      dim3 g1(x->colred_chunks, C);
+      k_colred_p1<<<g1, 256, 0, st>>>(x->R, in, s_in, O.rows, O.n_in, x->colred, x->colred_chunks);
+      k_colred_p2<<<C, 256, 0, st>>>(x->colred, x->colred_chunks, O.n_in, x->d_slot + O.w_off,
+                                     O.bias ? x->d_slot + O.b_off : nullptr, x->gl, x->k);
+      x->launches += 2;
+    }
+    if (nl - 1 > N.l_min) {
+      const LayerInfo& Pv = x->layers[N.layers[nl - 2]];
+      const int64_t total = (int64_t)C * Pv.rows * Pv.n_out;
+      const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+      k_rank1_dact<<<blocks, 256, 0, st>>>(x->R, x->Wd, x->P, O.w_off, Pv.A, Pv.D, Pv.act, Pv.rows, Pv.n_out,
+                                           C, N.G[0]);
+      x->launches++;
+      enqueue_backward_net(x, N, nl - 2, 0, st);
+    }
+    return;
+  }
+  // ---- DeepONet (factored over unique branch / trunk inputs, Q16) ----
+  for (int ni = 0; ni < 2; ++ni) {
+    NetInfo& N = x->nets[ni];
+    for (int i = 0; i < (int)N.layers.size(); ++i) enqueue_forward_hidden(x, N, i, st);
+  }
+  NetInfo& Nb = x->nets[0];
+  NetInfo& Nt = x->nets[1];
+  const LayerInfo& Bl = x->layers[Nb.layers.back()];
+  const LayerInfo& Tl = x->layers[Nt.layers.back()];
+  const int p = Bl.n_out;
+  {  // combine O = B T^T + b0, residual, R = (V - O)/sigma^2, partial sums
+    GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+    a.A = Bl.A; a.lda = p; a.sA = x->n_c * p;
+    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+    a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+    a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
+    if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
+    a.inv_s2 = 1.0 / (x->sigma * x->sigma);
+    a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
+    launch_gemm(x, a, true, true, st, "combine");
+  }
+  if (Nb.l_min >= 0) {  // dB = R T, times act' of the branch output layer
+    GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
+    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+    a.C = Nb.G[0]; a.ldc = p; a.sC = x->n_c * p;
+    a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = (Bl.act == ACT_SIN) ? Bl.D : Bl.A; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
+    launch_gemm(x, a, true, false, st, "dB");
+  }
+  if (Nt.l_min >= 0) {  // dT = R^T B, times act' of the trunk output layer
+    GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
+    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+    a.B = Bl.A; a.ldb = p; a.sB = x->n_c * p;
+    a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
+    a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
+    launch_gemm(x, a, false, false, st, "dT");
+  }
+  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+  if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+}
+
+void enqueue_reduce(hmc_ctx* x, cudaStream_t st, std::string& err) {
+  k_reduce_partials<<<x->C, KT, 0, st>>>(x->part_sq, x->part_r, x->n_part, x->lik, x->gl, x->k, x->b0_slot);
+  x->launches++;
+  if (x->mode == HMC_MODE_DATA && x->comm) {
+    CKN(ncclGroupStart());
+    CKN(ncclAllReduce(x->gl, x->gl, (size_t)(x->C * x->k), ncclFloat32, ncclSum, x->comm, st));
+    CKN(ncclAllReduce(x->lik, x->lik, (size_t)x->C, ncclFloat64, ncclSum, x->comm, st));
+    CKN(ncclGroupEnd());
+  }
+}
+
+// body + reduce + finalize for one gradient evaluation inside a trajectory
+void enqueue_step(hmc_ctx* x, int mode, cudaStream_t st, std::string& err) {
+  const int idb = prof_begin(x, st, true);
+  const double f0 = x->flop_acc;
+  enqueue_body(x, st);
+  x->body_flops = x->flop_acc - f0;
+  prof_end(x, idb, st, "body", x->body_flops, 0.0);
+  const int idr = prof_begin(x, st);
+  enqueue_reduce(x, st, err);
+  prof_end(x, idr, st, "reduce", 0.0, 0.0);
+  const int idf = prof_begin(x, st);
+  k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), mode);
+  x->launches++;
+  prof_end(x, idf, st, "finalize", 0.0, 0.0);
+}
+
+void capture_begin(hmc_ctx* x, std::string& err) {
+  CK(cudaStreamBeginCapture(x->st, cudaStreamCaptureModeThreadLocal));
+}
+
+cudaGraphExec_t capture_end(hmc_ctx* x, std::string& err) {
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamEndCapture(x->st, &g));
+  cudaGraphExec_t e = nullptr;
+  cudaError_t r = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  if (r != cudaSuccess) {
+    err = std::string("cudaGraphInstantiate: ") + cudaGetErrorString(r);
+    throw Fail{HMC_E_CUDA};
+  }
+  return e;
+}
+
+void build_grad_graph(hmc_ctx* x, std::string& err) {
+  if (x->grad_exec) return;
+  capture_begin(x, err);
+  const int64_t l0 = x->launches;
+  x->prof_armed = false;
+  try {
+    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->wrk_theta, x->d_idx, x->Wd, x->k, x->P, x->C);
+    x->launches++;
+    enqueue_body(x, x->st);
+    x->per_body = x->launches - l0 - 1;
+    enqueue_reduce(x, x->st, err);
+    k_finalize<<<x->C, KT, 0, x->st>>>(x->kstate(), 0);
+    x->launches++;
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(x->st, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  x->grad_exec = capture_end(x, err);
+}
+
+void build_traj_graph(hmc_ctx* x, int L, std::string& err) {
+  if (x->traj_exec && x->traj_L == L) return;
+  if (x->traj_exec) {
+    cudaGraphExecDestroy(x->traj_exec);
+    x->traj_exec = nullptr;
+  }
+  x->prof_clear();
+  capture_begin(x, err);
+  try {
+    x->prof_step = -1;
+    x->prof_armed = x->prof_on;
+    int id = prof_begin(x, x->st);
+    k_traj_begin<<<x->C, KT, 0, x->st>>>(x->kstate(), L == 0 ? 1 : 0);
+    prof_end(x, id, x->st, "traj_begin", 0.0, 0.0);
+    for (int s = 0; s < L; ++s) {
+      x->prof_step = s;
+      x->prof_armed = x->prof_on && s == 0;
+      enqueue_step(x, s == L - 1 ? 2 : 1, x->st, err);
+    }
+    x->prof_step = -1;
+    x->prof_armed = x->prof_on;
+    id = prof_begin(x, x->st);
+    k_mh<<<x->C, KT, 0, x->st>>>(x->kstate());
+    k_advance<<<1, 1, 0, x->st>>>(x->d_rec);
+    x->launches += 3;
+    prof_end(x, id, x->st, "mh", 0.0, 0.0);
+    x->prof_armed = false;
+  } catch (...) {
+    x->prof_armed = false;
+    cudaGraph_t g;
+    cudaStreamEndCapture(x->st, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  x->traj_exec = capture_end(x, err);
+  x->traj_L = L;
+}
+
+void sync_in(hmc_ctx* x, cudaStream_t user, std::string& err) {
+  CK(cudaEventRecord(x->ev_in, user));
+  CK(cudaStreamWaitEvent(x->st, x->ev_in, 0));
+}
+
+void sync_out(hmc_ctx* x, cudaStream_t user, bool host, std::string& err) {
+  if (host) {
+    CK(cudaStreamSynchronize(x->st));
+    return;
+  }
+  CK(cudaEventRecord(x->ev_out, x->st));
+  CK(cudaStreamWaitEvent(user, x->ev_out, 0));
+}
+
+void cpy(void* dst, const void* src, size_t bytes, cudaStream_t st, std::string& err) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+}
+
+void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, int64_t iter, double eps,
+             std::string& err) {
+  CK(cudaEventSynchronize(x->ev_stage));  // previous staging copy consumed
+  x->h_rec->samples = samples;
+  x->h_rec->acc = acc;
+  x->h_rec->dH = dH;
+  x->h_rec->S = S;
+  x->h_rec->sidx = 0;
+  x->h_rec->iter = iter;
+  *x->h_eps = eps;
+  CK(cudaMemcpyAsync(x->d_rec, x->h_rec, sizeof(Rec), cudaMemcpyHostToDevice, x->st));
+  CK(cudaMemcpyAsync(x->d_eps, x->h_eps, sizeof(double), cudaMemcpyHostToDevice, x->st));
+  CK(cudaEventRecord(x->ev_stage, x->st));
+}
+
+// ---------------------------------------------------------------------------------------------
+void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, std::string& err) {
+  CFG(arch && data && cfg, "arch, data and config must be non-NULL");
+  CFG(arch->kind == HMC_MLP || arch->kind == HMC_DEEPONET, "arch.kind must be HMC_MLP or HMC_DEEPONET");
+  x->kind = arch->kind;
+  x->n_nets = arch->kind == HMC_MLP ? 1 : 2;
+  CK(cudaGetDevice(&x->dev));
+  // ---- architecture and flat layout ----
+  int64_t off = 0;
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    const hmc_net& net = arch->net[ni];
+    CFG(net.n_layers >= 1 && net.widths && net.acts && net.has_bias, "net needs >= 1 layer and widths/acts/has_bias");
+    for (int l = 0; l < net.n_layers; ++l) {
+      CFG(net.widths[l] >= 1 && net.widths[l + 1] >= 1, "layer widths must be >= 1");
+      CFG(net.acts[l] >= 0 && net.acts[l] <= 2, "activation must be HMC_ACT_*");
+      LayerInfo L;
+      L.net = ni; L.l = l; L.n_in = net.widths[l]; L.n_out = net.widths[l + 1]; L.act = net.acts[l];
+      L.bias = net.has_bias[l] != 0;
+      L.w_off = off; off += (int64_t)L.n_in * L.n_out;
+      if (L.bias) { L.b_off = off; off += L.n_out; }
+      x->nets[ni].layers.push_back((int)x->layers.size());
+      x->nets[ni].max_w = std::max(x->nets[ni].max_w, std::max(L.n_in, L.n_out));
+      x->layers.push_back(L);
+    }
+  }
+  if (x->kind == HMC_MLP) {
+    const hmc_net& net = arch->net[0];
+    CFG(net.widths[net.n_layers] == 1, "MLP output width must be 1 (scalar regression, P:68)");
+    CFG(net.acts[net.n_layers - 1] == HMC_ACT_IDENTITY, "MLP output layer must be linear (identity)");
+  } else {
+    CFG(arch->net[0].widths[arch->net[0].n_layers] == arch->net[1].widths[arch->net[1].n_layers],
+        "DeepONet branch and trunk output widths must be equal (S:102)");
+    x->has_b0 = arch->has_b0 != 0;
+    if (x->has_b0) { x->b0_off = off; off += 1; }
+  }
+  x->P = off;
+  CFG(cfg->P == x->P, ("frozen length P=" + std::to_string(cfg->P) + " != parameter count " + std::to_string(x->P)).c_str());
+  // ---- config ----
+  CFG(cfg->k >= 1 && cfg->k <= x->P, "need 1 <= k <= P (an empty mask has nothing to sample)");
+  x->k = cfg->k;
+  CFG(std::isfinite(cfg->noise_sigma) && cfg->noise_sigma > 0, "noise_sigma must be finite and > 0");
+  CFG(std::isfinite(cfg->prior_sigma) && cfg->prior_sigma > 0, "prior_sigma must be finite and > 0");
+  x->sigma = cfg->noise_sigma;
+  x->sigma_p = cfg->prior_sigma;
+  CFG(cfg->n_chains >= 1 && cfg->n_chains <= 65535, "n_chains must be in [1, 65535]");
+  x->C = cfg->n_chains;
+  x->seed = cfg->seed;
+  CFG(cfg->frozen && cfg->idx, "frozen and idx must be non-NULL");
+  std::vector<float> h_frozen = to_host(cfg->frozen, (size_t)x->P, err);
+  std::vector<int32_t> h_idx = to_host(cfg->idx, (size_t)x->k, err);
+  for (int64_t j = 0; j < x->k; ++j) {
+    CFG(h_idx[j] >= 0 && h_idx[j] < x->P, "idx entries must lie in [0, P)");
+    CFG(j == 0 || h_idx[j] > h_idx[j - 1], "idx must be strictly ascending");
+  }
+  for (float v : h_frozen) CFG(std::isfinite(v), "frozen values must be finite");
+  std::vector<float> h_im;
+  if (cfg->inv_mass) {
+    h_im = to_host(cfg->inv_mass, (size_t)x->k, err);
+    for (float v : h_im) CFG(std::isfinite(v) && v > 0, "inv_mass entries must be finite and > 0");
+  }
+  std::vector<uint32_t> h_ch(x->C);
+  if (cfg->chain_ids) h_ch = to_host(cfg->chain_ids, (size_t)x->C, err);
+  else for (int c = 0; c < x->C; ++c) h_ch[c] = (uint32_t)c;
+  {
+    std::vector<uint32_t> s = h_ch;
+    std::sort(s.begin(), s.end());
+    for (size_t i = 1; i < s.size(); ++i) CFG(s[i] != s[i - 1], "chain ids must be unique");
+  }
+  CFG(cfg->mode >= 0 && cfg->mode <= 2, "mode must be HMC_MODE_*");
+  x->mode = cfg->mode;
+  x->rank = cfg->rank;
+  x->world = cfg->world;
+  CFG(x->world >= 1 && x->rank >= 0 && x->rank < x->world, "need 0 <= rank < world");
+  CFG(x->mode == HMC_MODE_DATA || x->world >= 1, "world");
+  // ---- data ----
+  std::vector<float> hx, hy, hu, hq, hv;
+  if (x->kind == HMC_MLP) {
+    CFG(data->x && data->y && data->n >= 1, "MLP data needs x, y and n >= 1");
+    x->n = data->n;
+    x->d_in = arch->net[0].widths[0];
+    hx = to_host(data->x, (size_t)(x->n * x->d_in), err);
+    hy = to_host(data->y, (size_t)x->n, err);
+    for (float v : hx) CFG(std::isfinite(v), "x must be finite");
+    for (float v : hy) CFG(std::isfinite(v), "y must be finite");
+    x->nets[0].rows = x->n;
+  } else {
+    CFG(data->u && data->q && data->v && data->n_c >= 1 && data->n_x >= 1, "DeepONet data needs u, q, v, n_c, n_x >= 1");
+    x->n_c = data->n_c;
+    x->n_x = data->n_x;
+    hu = to_host(data->u, (size_t)(x->n_c * arch->net[0].widths[0]), err);
+    hq = to_host(data->q, (size_t)(x->n_x * arch->net[1].widths[0]), err);
+    hv = to_host(data->v, (size_t)(x->n_c * x->n_x), err);
+    for (float v : hu) CFG(std::isfinite(v), "u must be finite");
+    for (float v : hq) CFG(std::isfinite(v), "q must be finite");
+    for (float v : hv) CFG(std::isfinite(v), "v must be finite");
+    x->nets[0].rows = x->n_c;
+    x->nets[1].rows = x->n_x;
+  }
+  const int64_t n_local = x->kind == HMC_MLP ? x->n : x->n_c * x->n_x;
+  x->n_global = data->n_global > 0 ? data->n_global : n_local;
+  if (x->mode != HMC_MODE_DATA || x->world == 1) CFG(x->n_global == n_local, "n_global must equal the local size outside DATA mode");
+  // ---- slot map, per-layer activity, l_min ----
+  std::vector<int32_t> slot((size_t)x->P, -1);
+  for (int64_t j = 0; j < x->k; ++j) slot[h_idx[j]] = (int32_t)j;
+  for (auto& L : x->layers) {
+    for (int64_t t = L.w_off; t < L.w_off + (int64_t)L.n_in * L.n_out && !L.any_active; ++t) L.any_active |= slot[t] >= 0;
+    if (L.bias) for (int t = 0; t < L.n_out && !L.any_active; ++t) L.any_active |= slot[L.b_off + t] >= 0;
+  }
+  if (x->has_b0) x->b0_slot = slot[x->b0_off];
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    NetInfo& N = x->nets[ni];
+    for (int i = 0; i < (int)N.layers.size(); ++i)
+      if (x->layers[N.layers[i]].any_active) { N.l_min = i; break; }
+  }
+  // ---- device allocations ----
+  const int C = x->C;
+  x->d_idx = dalloc<int32_t>(x, x->k, err);
+  x->d_slot = dalloc<int32_t>(x, x->P, err);
+  x->d_chain = dalloc<uint32_t>(x, C, err);
+  if (!h_im.empty()) x->d_inv_mass = dalloc<float>(x, x->k, err);
+  x->Wd = dalloc<float>(x, (size_t)C * x->P, err);
+  CK(cudaMemcpy(x->d_idx, h_idx.data(), x->k * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(x->d_slot, slot.data(), x->P * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(x->d_chain, h_ch.data(), C * 4, cudaMemcpyHostToDevice));
+  if (!h_im.empty()) CK(cudaMemcpy(x->d_inv_mass, h_im.data(), x->k * 4, cudaMemcpyHostToDevice));
+  for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
+  const size_t Ck = (size_t)C * x->k;
+  x->cur_theta = dalloc<float>(x, Ck, err);
+  x->cur_grad = dalloc<float>(x, Ck, err);
+  x->wrk_theta = dalloc<float>(x, Ck, err);
+  x->wrk_grad = dalloc<float>(x, Ck, err);
+  x->p = dalloc<float>(x, Ck, err);
+  x->gl = dalloc<float>(x, Ck, err);
+  x->cur_logp = dalloc<double>(x, C, err);
+  x->wrk_logp = dalloc<double>(x, C, err);
+  x->H0 = dalloc<double>(x, C, err);
+  x->lik = dalloc<double>(x, C, err);
+  x->d_eps = dalloc<double>(x, 1, err);
+  x->d_rec = dalloc<Rec>(x, 1, err);
+  x->tmp_acc = dalloc<uint8_t>(x, C, err);
+  x->tmp_dH = dalloc<double>(x, C, err);
+  if (x->kind == HMC_MLP) {
+    x->d_x = dalloc<float>(x, hx.size(), err);
+    x->d_y = dalloc<float>(x, hy.size(), err);
+    CK(cudaMemcpy(x->d_x, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(x->d_y, hy.data(), hy.size() * 4, cudaMemcpyHostToDevice));
+    x->nets[0].input = x->d_x;
+    x->n_part = (int)((x->n + 63) / 64);
+    x->R = dalloc<float>(x, (size_t)C * x->n, err);
+    const LayerInfo& O = x->layers[x->nets[0].layers.back()];
+    x->colred_chunks = (int)((x->n + COLRED_CH - 1) / COLRED_CH);
+    x->colred = dalloc<float>(x, (size_t)C * x->colred_chunks * (O.n_in + 1), err);
+  } else {
+    x->d_u = dalloc<float>(x, hu.size(), err);
+    x->d_q = dalloc<float>(x, hq.size(), err);
+    x->d_v = dalloc<float>(x, hv.size(), err);
+    CK(cudaMemcpy(x->d_u, hu.data(), hu.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(x->d_q, hq.data(), hq.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(x->d_v, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice));
+    x->nets[0].input = x->d_u;
+    x->nets[1].input = x->d_q;
+    x->R = dalloc<float>(x, (size_t)C * x->n_c * x->n_x, err);
+    const int p = x->layers[x->nets[0].layers.back()].n_out;
+    GemmArgs probe = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+    probe.epi = EPI_RESID;
+    x->n_part = x->tc.n_tiles(probe, true, true);
+    if (x->n_part <= 0) {
+      const int bm = pick_bm((int)x->n_c, (int)x->n_x);
+      x->n_part = (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm));
+    }
+  }
+  x->part_sq = dalloc<double>(x, (size_t)C * x->n_part, err);
+  x->part_r = dalloc<double>(x, (size_t)C * x->n_part, err);
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    NetInfo& N = x->nets[ni];
+    const int nl = (int)N.layers.size();
+    for (int i = 0; i < nl; ++i) {
+      LayerInfo& L = x->layers[N.layers[i]];
+      L.rows = N.rows;
+      const bool mlp_out = (x->kind == HMC_MLP && i == nl - 1);
+      if (!mlp_out) L.A = dalloc<float>(x, (size_t)C * L.rows * L.n_out, err);
+      if (L.act == ACT_SIN && !mlp_out) L.D = dalloc<float>(x, (size_t)C * L.rows * L.n_out, err);
+    }
+    if (N.l_min >= 0) {
+      N.G[0] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
+      N.G[1] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
+    }
+  }
+  CK(cudaMallocHost((void**)&x->h_rec, sizeof(Rec)));
+  CK(cudaMallocHost((void**)&x->h_eps, sizeof(double)));
+  CK(cudaEventCreateWithFlags(&x->ev_stage, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
+  CK(cudaEventRecord(x->ev_stage, 0));
+  CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
+  // ---- NCCL (DATA mode) ----
+  if (x->mode == HMC_MODE_DATA && x->world > 1) {
+    CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, sizeof(id));
+    CKN(ncclCommInitRank(&x->comm, x->world, id, x->rank));
+  }
+  x->engine = x->tc.describe();
+  CK(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+#define API_BEGIN(ctx)                                                                        \
+  if (!(ctx)) {                                                                               \
+    g_err = "NULL context";                                                                   \
+    return HMC_E_STATE;                                                                       \
+  }                                                                                           \
+  std::string& err = (ctx)->err;                                                              \
+  try {                                                                                       \
+    CK(cudaSetDevice((ctx)->dev));
+
+#define API_END                                                                               \
+  }                                                                                           \
+  catch (Fail f) {                                                                            \
+    return f.code;                                                                            \
+  }                                                                                           \
+  return HMC_OK;
+
+extern "C" {
+
+int hmc_comm_unique_id(uint8_t id_out[128]) {
+  if (!id_out) {
+    g_err = "id_out is NULL";
+    return HMC_E_CONFIG;
+  }
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return HMC_E_NCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(id_out, &id, 128);
+  return HMC_OK;
+}
+
+int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, void* stream, hmc_ctx** out) {
+  (void)stream;
+  if (!out) {
+    g_err = "out is NULL";
+    return HMC_E_CONFIG;
+  }
+  *out = nullptr;
+  std::unique_ptr<hmc_ctx> x(new hmc_ctx());
+  try {
+    setup_impl(x.get(), arch, data, cfg, x->err);
+  } catch (Fail f) {
+    g_err = x->err;
+    return f.code;
+  }
+  *out = x.release();
+  return HMC_OK;
+}
+
+int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream) {
+  API_BEGIN(ctx)
+  CFG(theta && logp && grad, "theta, logp and grad must be non-NULL");
+  cudaStream_t us = (cudaStream_t)stream;
+  const bool host = !is_device_ptr(theta) || !is_device_ptr(logp) || !is_device_ptr(grad);
+  build_grad_graph(ctx, err);
+  sync_in(ctx, us, err);
+  const size_t Ck = (size_t)ctx->C * ctx->k;
+  cpy(ctx->wrk_theta, theta, Ck * 4, ctx->st, err);
+  CK(cudaGraphLaunch(ctx->grad_exec, ctx->st));
+  cpy(grad, ctx->wrk_grad, Ck * 4, ctx->st, err);
+  cpy(logp, ctx->wrk_logp, ctx->C * 8, ctx->st, err);
+  sync_out(ctx, us, host, err);
+  API_END
+}
+
+int hmc_logpost_const(const hmc_ctx* ctx, double* c) {
+  if (!ctx) { g_err = "NULL context"; return HMC_E_STATE; }
+  if (!c) return HMC_E_CONFIG;
+  const double l2pi = std::log(2.0 * M_PI);
+  *c = -(double)ctx->n_global * (std::log(ctx->sigma) + 0.5 * l2pi) - (double)ctx->k * (std::log(ctx->sigma_p) + 0.5 * l2pi);
+  return HMC_OK;
+}
+
+static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
+                    int32_t S, float* samples, uint8_t* acc, double* dH, void* stream) {
+  API_BEGIN(ctx)
+  CFG(theta && logp && grad, "theta, logp and grad must be non-NULL");
+  CFG(std::isfinite(eps) && eps > 0, "eps must be finite and > 0");
+  CFG(L >= 0, "L must be >= 0");
+  CFG(S >= 1, "S must be >= 1");
+  CFG(iter0 >= 0 && iter0 + S <= (int64_t)1 << 32, "iter must lie in [0, 2^32)");
+  cudaStream_t us = (cudaStream_t)stream;
+  const size_t Ck = (size_t)ctx->C * ctx->k;
+  bool host = !is_device_ptr(theta) || !is_device_ptr(logp) || !is_device_ptr(grad);
+  // output records: device pointers are written in place, host ones staged in device temps
+  float* d_samples = nullptr;
+  uint8_t* d_acc = nullptr;
+  double* d_dH = nullptr;
+  DevBuf tmp;
+  auto tmp_alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    tmp.ptrs.push_back(p);
+    return p;
+  };
+  if (samples) {
+    if (is_device_ptr(samples)) d_samples = samples;
+    else { host = true; d_samples = (float*)tmp_alloc(Ck * S * 4); }
+  }
+  if (acc) {
+    if (is_device_ptr(acc)) d_acc = acc;
+    else { host = true; d_acc = (S == 1) ? ctx->tmp_acc : (uint8_t*)tmp_alloc((size_t)ctx->C * S); }
+  }
+  if (dH) {
+    if (is_device_ptr(dH)) d_dH = dH;
+    else { host = true; d_dH = (S == 1) ? ctx->tmp_dH : (double*)tmp_alloc((size_t)ctx->C * S * 8); }
+  }
+  build_traj_graph(ctx, L, err);
+  sync_in(ctx, us, err);
+  cpy(ctx->cur_theta, theta, Ck * 4, ctx->st, err);
+  cpy(ctx->cur_grad, grad, Ck * 4, ctx->st, err);
+  cpy(ctx->cur_logp, logp, ctx->C * 8, ctx->st, err);
+  set_rec(ctx, d_samples, d_acc, d_dH, S, iter0, eps, err);
+  for (int s = 0; s < S; ++s) CK(cudaGraphLaunch(ctx->traj_exec, ctx->st));
+  cpy(theta, ctx->cur_theta, Ck * 4, ctx->st, err);
+  cpy(grad, ctx->cur_grad, Ck * 4, ctx->st, err);
+  cpy(logp, ctx->cur_logp, ctx->C * 8, ctx->st, err);
+  if (samples && d_samples != samples) cpy(samples, d_samples, Ck * S * 4, ctx->st, err);
+  if (acc && d_acc != acc) cpy(acc, d_acc, (size_t)ctx->C * S, ctx->st, err);
+  if (dH && d_dH != dH) cpy(dH, d_dH, (size_t)ctx->C * S * 8, ctx->st, err);
+  sync_out(ctx, us, host || !tmp.ptrs.empty(), err);
+  API_END
+}
+
+int hmc_trajectory(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter,
+                   uint8_t* acc, double* dH, void* stream) {
+  return run_traj(ctx, theta, logp, grad, eps, L, iter, 1, nullptr, acc, dH, stream);
+}
+
+int hmc_sample(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
+               int32_t S, float* samples, uint8_t* acc, double* dH, void* stream) {
+  return run_traj(ctx, theta, logp, grad, eps, L, iter0, S, samples, acc, dH, stream);
+}
+
+int hmc_destroy(hmc_ctx* ctx) {
+  if (!ctx) return HMC_OK;
+  cudaSetDevice(ctx->dev);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  delete ctx;
+  return HMC_OK;
+}
+
+const char* hmc_last_error(const hmc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int hmc_launch_counts(const hmc_ctx* ctx, int64_t* per_grad, int64_t* per_traj_base, int64_t* per_step) {
+  if (!ctx) { g_err = "NULL context"; return HMC_E_STATE; }
+  hmc_ctx* x = const_cast<hmc_ctx*>(ctx);
+  if (!x->grad_exec) {
+    // count without executing: the body's launch count is static for a context
+    std::string& err = x->err;
+    try {
+      CK(cudaSetDevice(x->dev));
+      build_grad_graph(x, err);
+    } catch (Fail f) {
+      return f.code;
+    }
+  }
+  if (per_grad) *per_grad = x->per_body + 3;
+  if (per_traj_base) *per_traj_base = 3;
+  if (per_step) *per_step = x->per_body + 2;
+  return HMC_OK;
+}
+
+int hmc_philox_words(uint64_t seed, uint32_t tag, uint32_t iter, uint32_t chain, int64_t nblocks, uint32_t* out,
+                     void* stream) {
+  if (!out || nblocks < 0) { g_err = "bad arguments"; return HMC_E_CONFIG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool dev = is_device_ptr(out);
+  uint32_t* d = out;
+  if (!dev && cudaMalloc(&d, (size_t)nblocks * 16 + 16) != cudaSuccess) { g_err = "cudaMalloc"; return HMC_E_OOM; }
+  k_philox_words<<<148 * 4, 256, 0, st>>>((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), tag, iter, chain,
+                                          nblocks, d);
+  cudaError_t e = cudaGetLastError();
+  if (!dev) {
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)nblocks * 16, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+  }
+  if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return HMC_E_CUDA; }
+  return HMC_OK;
+}
+
+int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream) {
+  API_BEGIN(ctx)
+  CFG(p && iter >= 0 && iter < ((int64_t)1 << 32), "p non-NULL, 0 <= iter < 2^32");
+  cudaStream_t us = (cudaStream_t)stream;
+  const bool host = !is_device_ptr(p);
+  sync_in(ctx, us, err);
+  k_momentum<<<ctx->C, KT, 0, ctx->st>>>(ctx->kstate(), (uint32_t)iter, ctx->p);
+  CK(cudaGetLastError());
+  cpy(p, ctx->p, (size_t)ctx->C * ctx->k * 4, ctx->st, err);
+  sync_out(ctx, us, host, err);
+  API_END
+}
+
+const char* hmc_engine_info(const hmc_ctx* ctx) { return ctx ? ctx->engine.c_str() : ""; }
+
+int hmc_profile(hmc_ctx* ctx, int32_t enable) {
+  API_BEGIN(ctx)
+  if ((enable != 0) != ctx->prof_on) {
+    ctx->prof_on = enable != 0;
+    if (ctx->traj_exec) {
+      CK(cudaStreamSynchronize(ctx->st));
+      cudaGraphExecDestroy(ctx->traj_exec);
+      ctx->traj_exec = nullptr;
+      ctx->traj_L = -1;
+    }
+  }
+  API_END
+}
+
+int hmc_profile_read(hmc_ctx* ctx, int32_t max_recs, hmc_prof_rec* out, int32_t* n_out) {
+  API_BEGIN(ctx)
+  CFG(n_out && (out || max_recs == 0), "n_out must be non-NULL");
+  CK(cudaStreamSynchronize(ctx->st));
+  const int n = (int)ctx->prof.size();
+  *n_out = n;
+  for (int i = 0; i < n && i < max_recs; ++i) {
+    const auto& r = ctx->prof[i];
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) {
+      cudaGetLastError();
+      ms = -1.f;
+    }
+    memset(out[i].name, 0, sizeof(out[i].name));
+    strncpy(out[i].name, r.name.c_str(), sizeof(out[i].name) - 1);
+    out[i].ms = ms;
+    out[i].flops = r.flops;
+    out[i].bytes = r.bytes;
+    out[i].step = r.step;
+  }
+  API_END
+}
+
+}  // extern "C"

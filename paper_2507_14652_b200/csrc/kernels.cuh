@@ -1,0 +1,312 @@
+// Non-GEMM kernels of the hot path (libhmc, sm_100a): output layer + likelihood reduction,
+// rank-1 input gradient, output-layer weight gradient, partial-sum reduction, and the
+// leapfrog / momentum / Metropolis kernels.  Citations: PAPER.md P:n, DESIGN.md §3 readings.
+#pragma once
+#include "common.cuh"
+
+namespace hmc {
+
+// Device-side record of hmc_sample progress (written by k_mh / k_advance inside the graph).
+struct Rec {
+  float* samples;   // [C x S x k] or nullptr
+  uint8_t* acc;     // [C x S] or nullptr
+  double* dH;       // [C x S] or nullptr
+  int64_t S;
+  int64_t sidx;     // current sample slot
+  int64_t iter;     // Philox iteration counter
+};
+
+// Everything the per-chain state kernels need.
+struct KState {
+  int C;
+  int64_t k, P;
+  const int32_t* idx;
+  const float* inv_mass;       // nullptr = identity
+  const uint32_t* chain_ids;
+  float* Wd;                   // [C x P] dense per-chain parameters (frozen mu + active theta)
+  float* cur_theta; float* cur_grad; double* cur_logp;   // chain state (the cache)
+  float* wrk_theta; float* wrk_grad; double* wrk_logp;   // trajectory working state
+  float* p; double* H0;
+  const float* gl;             // [C x k] likelihood part of the gradient
+  const double* lik;           // [C] sum of squared residuals
+  double inv_2s2;              // 1 / (2 sigma^2)
+  double inv_sp2;              // 1 / sigma_p^2
+  const double* eps;           // device scalar step size
+  Rec* rec;
+  uint32_t key0, key1;
+};
+
+constexpr int KT = 256;  // threads of the per-chain state kernels
+
+// ---- scatter theta_s into the dense per-chain parameter vector (Theta_~s = mu_~s) --
+__global__ void k_scatter(const float* __restrict__ theta, const int32_t* __restrict__ idx,
+                          float* __restrict__ Wd, int64_t k, int64_t P, int C) {
+  const int64_t total = (int64_t)C * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / k, j = t - c * k;
+    Wd[c * P + idx[j]] = theta[t];
+  }
+}
+
+// ---- MLP output layer (width 1, identity): f = A w + b; r = y - f; R = r / sigma^2;
+//      fp64 partial sums of r^2 per 64-row block (likelihood P:564) ----
+__global__ void __launch_bounds__(256) k_out_fwd(const float* __restrict__ Ain, int64_t sA, int n_in,
+                                                 int64_t rows, const float* __restrict__ Wd, int64_t P,
+                                                 int64_t w_off, int64_t b_off, const float* __restrict__ y,
+                                                 float* __restrict__ R, double inv_s2,
+                                                 double* __restrict__ part_sq, int n_part) {
+  extern __shared__ float w_s[];
+  __shared__ double red[8];
+  const int c = blockIdx.y;
+  const float* w = Wd + (int64_t)c * P + w_off;
+  for (int j = threadIdx.x; j < n_in; j += blockDim.x) w_s[j] = w[j];
+  const float bias = (b_off >= 0) ? Wd[(int64_t)c * P + b_off] : 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* A = Ain + (int64_t)c * sA;
+  double psq = 0.0;
+  for (int rr = 0; rr < 8; ++rr) {
+    const int64_t n = (int64_t)blockIdx.x * 64 + warp * 8 + rr;
+    if (n >= rows) break;
+    float s = 0.f;
+    for (int j = lane; j < n_in; j += 32) s = fmaf(A[n * n_in + j], w_s[j], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const float f = s + bias;
+      const float r = y[n] - f;
+      R[(int64_t)c * rows + n] = (float)((double)r * inv_s2);
+      psq += (double)r * (double)r;
+    }
+  }
+  const double tot = block_sum_d<256>(psq, red);
+  if (threadIdx.x == 0) part_sq[(int64_t)c * n_part + blockIdx.x] = tot;
+}
+
+// ---- input gradient of the width-1 output layer: G[n, j] = R[n] w[j] act'(A[n, j]) ----
+__global__ void k_rank1_dact(const float* __restrict__ R, const float* __restrict__ Wd, int64_t P,
+                             int64_t w_off, const float* __restrict__ Aprev, const float* __restrict__ Dprev,
+                             int act, int64_t rows, int n_in, int C, float* __restrict__ G) {
+  const int64_t per = rows * n_in, total = per * C;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / per, rem = t - c * per, n = rem / n_in;
+    const int j = (int)(rem - n * n_in);
+    float v = R[c * rows + n] * Wd[c * P + w_off + j];
+    if (act == ACT_TANH) { const float a = Aprev[t]; v *= (1.f - a * a); }
+    else if (act == ACT_SIN) v *= Dprev[t];
+    G[t] = v;
+  }
+}
+
+// ---- weight gradient of the width-1 output layer, pass 1: per 256-row chunk,
+//      part[c][chunk][j] = sum_n R[n] X[n, j] (j < n_in), and sum_n R[n] at j = n_in ----
+constexpr int COLRED_CH = 256;
+__global__ void k_colred_p1(const float* __restrict__ R, const float* __restrict__ X, int64_t sX,
+                            int64_t rows, int n_in, float* __restrict__ part, int n_chunks) {
+  const int c = blockIdx.y, ch = blockIdx.x;
+  const float* Xc = X + (int64_t)c * sX;
+  const float* Rc = R + (int64_t)c * rows;
+  const int64_t n0 = (int64_t)ch * COLRED_CH;
+  const int64_t n1 = min(rows, n0 + COLRED_CH);
+  for (int j = threadIdx.x; j <= n_in; j += blockDim.x) {
+    float s = 0.f;
+    if (j < n_in) {
+      for (int64_t n = n0; n < n1; ++n) s = fmaf(Rc[n], Xc[n * n_in + j], s);
+    } else {
+      for (int64_t n = n0; n < n1; ++n) s += Rc[n];
+    }
+    part[((int64_t)c * n_chunks + ch) * (n_in + 1) + j] = s;
+  }
+}
+
+// pass 2: fixed-order sum over chunks, compaction into the k-vector through the slot map
+__global__ void k_colred_p2(const float* __restrict__ part, int n_chunks, int n_in,
+                            const int32_t* __restrict__ slot_w, const int32_t* __restrict__ slot_b,
+                            float* __restrict__ gl, int64_t k) {
+  const int c = blockIdx.x;
+  for (int j = threadIdx.x; j <= n_in; j += blockDim.x) {
+    const int s = (j < n_in) ? slot_w[j] : (slot_b ? slot_b[0] : -1);
+    if (s < 0) continue;
+    float acc = 0.f;
+    for (int ch = 0; ch < n_chunks; ++ch) acc += part[((int64_t)c * n_chunks + ch) * (n_in + 1) + j];
+    gl[(int64_t)c * k + s] = acc;
+  }
+}
+
+// ---- per-chain fixed-order reduction of the likelihood partials: lik[c] = sum r^2; the
+//      DeepONet output-bias gradient sum_n R_n goes to its k-slot ----
+__global__ void __launch_bounds__(KT) k_reduce_partials(const double* __restrict__ part_sq,
+                                                        const double* __restrict__ part_r, int n_part,
+                                                        double* __restrict__ lik, float* __restrict__ gl,
+                                                        int64_t k, int b0_slot) {
+  __shared__ double red[KT / 32];
+  const int c = blockIdx.x;
+  double s = 0.0, r = 0.0;
+  for (int t = threadIdx.x; t < n_part; t += KT) {
+    s += part_sq[(int64_t)c * n_part + t];
+    if (b0_slot >= 0) r += part_r[(int64_t)c * n_part + t];
+  }
+  s = block_sum_d<KT>(s, red);
+  if (b0_slot >= 0) r = block_sum_d<KT>(r, red);
+  if (threadIdx.x == 0) {
+    lik[c] = s;
+    if (b0_slot >= 0) gl[(int64_t)c * k + b0_slot] = (float)r;
+  }
+}
+
+// ---- finalize a gradient evaluation: g = g_lik - theta / sigma_p^2 (prior P:233, Q8),
+//      log pi = -sum r^2 / (2 sigma^2) - sum theta^2 / (2 sigma_p^2) (fp64);
+//      mode 0: plain (hmc_grad); 1: + full kick p += eps g, drift theta += eps M^-1 p and
+//      scatter (an inner leapfrog step, Q2); 2: + closing half kick p += eps/2 g ----
+__global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
+  __shared__ double red[KT / 32];
+  const int c = blockIdx.x;
+  const double eps = (mode != 0) ? *s.eps : 0.0;
+  const float fe = (float)eps, fh = (float)(0.5 * eps);
+  double ss = 0.0;
+  for (int64_t j = threadIdx.x; j < s.k; j += KT) {
+    const int64_t t = (int64_t)c * s.k + j;
+    float th = s.wrk_theta[t];
+    const float g = s.gl[t] - (float)((double)th * s.inv_sp2);
+    s.wrk_grad[t] = g;
+    ss += (double)th * (double)th;
+    if (mode == 1) {
+      const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+      const float p = fmaf(fe, g, s.p[t]);
+      s.p[t] = p;
+      th = fmaf(fe * im, p, th);
+      s.wrk_theta[t] = th;
+      s.Wd[(int64_t)c * s.P + s.idx[j]] = th;
+    } else if (mode == 2) {
+      s.p[t] = fmaf(fh, g, s.p[t]);
+    }
+  }
+  ss = block_sum_d<KT>(ss, red);
+  if (threadIdx.x == 0) s.wrk_logp[c] = -s.lik[c] * s.inv_2s2 - 0.5 * ss * s.inv_sp2;
+}
+
+// ---- start of a trajectory (Algorithm 2): p = sqrt(m) z with z from Philox
+//      (key = seed, counter = (j>>2, tag 0, iter, chain_id)), K0 = 1/2 sum p^2 / m (fp64),
+//      H0 = -log pi(theta) + K0; then the opening half kick and first drift (+ scatter).
+//      L0 != 0: identity trajectory (no kick / drift; working state = current state) ----
+__global__ void __launch_bounds__(KT) k_traj_begin(KState s, int L0) {
+  __shared__ double red[KT / 32];
+  const int c = blockIdx.x;
+  const uint32_t iter = (uint32_t)s.rec->iter;
+  const uint32_t chain = s.chain_ids[c];
+  const double eps = *s.eps;
+  const float fe = (float)eps, fh = (float)(0.5 * eps);
+  double K0 = 0.0;
+  const int64_t nb = (s.k + 3) / 4;
+  for (int64_t blk = threadIdx.x; blk < nb; blk += KT) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)blk, 0u, iter, chain), s.key0, s.key1);
+    double z[4];
+    box_muller4(w, z);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int64_t j = blk * 4 + l;
+      if (j >= s.k) break;
+      const int64_t t = (int64_t)c * s.k + j;
+      const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+      float p = (float)(sqrt(1.0 / (double)im) * z[l]);
+      K0 += 0.5 * (double)p * (double)p * (double)im;
+      float th = s.cur_theta[t];
+      if (L0) {
+        s.wrk_grad[t] = s.cur_grad[t];
+      } else {
+        p = fmaf(fh, s.cur_grad[t], p);
+        th = fmaf(fe * im, p, th);
+        s.Wd[(int64_t)c * s.P + s.idx[j]] = th;
+      }
+      s.p[t] = p;
+      s.wrk_theta[t] = th;
+    }
+  }
+  K0 = block_sum_d<KT>(K0, red);
+  if (threadIdx.x == 0) {
+    s.H0[c] = -s.cur_logp[c] + K0;
+    if (L0) s.wrk_logp[c] = s.cur_logp[c];
+  }
+}
+
+// ---- Metropolis-Hastings: H* = -log pi(theta*) + K(p*); u from Philox tag 1
+//      word 0; accept iff ln u < H0 - H* (strict; NaN rejects, Q4/Q5).  On accept the
+//      working state becomes the chain state; the (possibly repeated) state is recorded ----
+__global__ void __launch_bounds__(KT) k_mh(KState s) {
+  __shared__ double red[KT / 32];
+  __shared__ int acc_s;
+  const int c = blockIdx.x;
+  double K1 = 0.0;
+  for (int64_t j = threadIdx.x; j < s.k; j += KT) {
+    const float p = s.p[(int64_t)c * s.k + j];
+    const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+    K1 += 0.5 * (double)p * (double)p * (double)im;
+  }
+  K1 = block_sum_d<KT>(K1, red);
+  Rec* rec = s.rec;
+  const int64_t sidx = rec->sidx;
+  if (threadIdx.x == 0) {
+    const double H1 = -s.wrk_logp[c] + K1;
+    const double H0 = s.H0[c];
+    const uint4 w = philox4x32_10(make_uint4(0u, 1u, (uint32_t)rec->iter, s.chain_ids[c]), s.key0, s.key1);
+    const double lu = log(u01(w.x));
+    const int acc = (isfinite(H1) && (lu < H0 - H1)) ? 1 : 0;
+    acc_s = acc;
+    if (acc) s.cur_logp[c] = s.wrk_logp[c];
+    if (rec->acc) rec->acc[(int64_t)c * rec->S + sidx] = (uint8_t)acc;
+    if (rec->dH) rec->dH[(int64_t)c * rec->S + sidx] = H1 - H0;
+  }
+  __syncthreads();
+  const int acc = acc_s;
+  for (int64_t j = threadIdx.x; j < s.k; j += KT) {
+    const int64_t t = (int64_t)c * s.k + j;
+    float th;
+    if (acc) {
+      th = s.wrk_theta[t];
+      s.cur_theta[t] = th;
+      s.cur_grad[t] = s.wrk_grad[t];
+    } else {
+      th = s.cur_theta[t];
+    }
+    if (rec->samples) rec->samples[((int64_t)c * rec->S + sidx) * s.k + j] = th;
+  }
+}
+
+__global__ void k_advance(Rec* rec) {
+  rec->sidx += 1;
+  rec->iter += 1;
+}
+
+// ---- diagnostics ----
+__global__ void k_philox_words(uint32_t k0, uint32_t k1, uint32_t tag, uint32_t iter, uint32_t chain,
+                               int64_t nblocks, uint32_t* __restrict__ out) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nblocks;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)b, tag, iter, chain), k0, k1);
+    out[4 * b + 0] = w.x;
+    out[4 * b + 1] = w.y;
+    out[4 * b + 2] = w.z;
+    out[4 * b + 3] = w.w;
+  }
+}
+
+__global__ void k_momentum(KState s, uint32_t iter, float* __restrict__ out) {
+  const int c = blockIdx.x;
+  const uint32_t chain = s.chain_ids[c];
+  const int64_t nb = (s.k + 3) / 4;
+  for (int64_t blk = threadIdx.x; blk < nb; blk += blockDim.x) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)blk, 0u, iter, chain), s.key0, s.key1);
+    double z[4];
+    box_muller4(w, z);
+    for (int l = 0; l < 4; ++l) {
+      const int64_t j = blk * 4 + l;
+      if (j >= s.k) break;
+      const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+      out[(int64_t)c * s.k + j] = (float)(sqrt(1.0 / (double)im) * z[l]);
+    }
+  }
+}
+
+}  // namespace hmc
