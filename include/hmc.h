@@ -179,6 +179,15 @@ typedef struct {
   int32_t step;
 } hmc_prof_rec;
 int hmc_profile(hmc_ctx* ctx, int32_t enable);
+
+/* One chain-batched GEMM C[b] (M x N) = A[b] (M x K) . B[b] (K x N) on a chosen engine
+ * (0 = SIMT FP32, 1 = tcgen05 3xTF32), no epilogue; device pointers, fp32 row-major with the
+ * given leading dimensions and per-batch strides.  A(m,k) = A[m*lda+k] if a_kmajor else
+ * A[k*lda+m]; B(k,n) = B[n*ldb+k] if b_kmajor else B[k*ldb+n].  HMC_E_CONFIG if the engine
+ * does not take the shape.  Used by the engine unit tests. */
+int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M, int32_t N, int32_t K,
+                   int32_t batch, const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb,
+                   int64_t sB, float* C, int64_t ldc, int64_t sC, void* stream);
 int hmc_profile_read(hmc_ctx* ctx, int32_t max_recs, hmc_prof_rec* out, int32_t* n_out);
 
 #ifdef __cplusplus

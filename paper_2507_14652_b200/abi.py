@@ -53,7 +53,7 @@ class hmc_config(ctypes.Structure):
 
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
-           "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read"]
+           "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -89,6 +89,8 @@ def lib():
     L.hmc_engine_info.argtypes = [vp]
     L.hmc_engine_info.restype = ctypes.c_char_p
     L.hmc_profile.argtypes = [vp, i32]
+    L.hmc_debug_gemm.argtypes = [i32, i32, i32, i32, i32, i32, i32, vp, i64, i64, vp, i64, i64, vp, i64,
+                                 i64, vp]
     L.hmc_profile_read.argtypes = [vp, i32, ctypes.POINTER(hmc_prof_rec), ctypes.POINTER(i32)]
     for name in EXPORTS:
         if name not in ("hmc_last_error", "hmc_engine_info"):
@@ -201,6 +203,14 @@ def hmc_momentum(ctx, it, out, stream=None):
 
 def hmc_engine_info(ctx) -> str:
     return lib().hmc_engine_info(ctx).decode()
+
+
+def hmc_debug_gemm(engine, a_kmajor, b_kmajor, M, N, K, batch, A, lda, sA, B, ldb, sB, C, ldc, sC,
+                   stream=None):
+    keep = []
+    _check(lib().hmc_debug_gemm(int(engine), int(a_kmajor), int(b_kmajor), M, N, K, batch,
+                                _ptr(A, keep), lda, sA, _ptr(B, keep), ldb, sB, _ptr(C, keep), ldc, sC,
+                                _stream(stream)))
 
 
 def hmc_profile(ctx, enable: bool):

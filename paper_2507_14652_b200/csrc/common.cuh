@@ -41,6 +41,13 @@ __device__ __forceinline__ void box_muller4(uint4 w, double z[4]) {
   z[3] = r23 * s;
 }
 
+// TF32 hi part, round-to-nearest-away (cvt.rna), as a float bit pattern with 13 zero low bits
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == ACT_TANH) return tanhf(z);
   if (act == ACT_SIN) return sinf(z);

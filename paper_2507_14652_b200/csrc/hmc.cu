@@ -34,6 +34,9 @@ struct LayerInfo {
   int net = 0, l = 0, n_in = 0, n_out = 0, act = 0;
   bool bias = false, any_active = false;
   int64_t w_off = 0, b_off = -1, rows = 0;
+  bool tc_w = false;          // weights kept as tf32 hi/lo planes for the tensor-core engine
+  bool bias_active = false;
+  int64_t q_off = 0;           // offset of this layer's weights in the hi/lo planes
   float* A = nullptr;  // [C x rows x n_out] layer output (hidden layers)
   float* D = nullptr;  // [C x rows x n_out] cos(z) for sin layers
 };
@@ -72,6 +75,10 @@ struct hmc_ctx {
   DevBuf mem;
   float *d_x = nullptr, *d_y = nullptr, *d_u = nullptr, *d_q = nullptr, *d_v = nullptr;
   float* Wd = nullptr;
+  float *Whi = nullptr, *Wlo = nullptr;
+  int64_t* d_tcpos = nullptr;
+  int64_t Ptc = 0;
+  int colred_cap = 0;
   int32_t *d_idx = nullptr, *d_slot = nullptr;
   float* d_inv_mass = nullptr;
   uint32_t* d_chain = nullptr;
@@ -127,7 +134,7 @@ struct hmc_ctx {
   KState kstate() const {
     KState s;
     s.C = C; s.k = k; s.P = P; s.idx = d_idx; s.inv_mass = d_inv_mass; s.chain_ids = d_chain;
-    s.Wd = Wd; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
+    s.Wd = Wd; s.Whi = Whi; s.Wlo = Wlo; s.tcpos = d_tcpos; s.Ptc = Ptc; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
     s.wrk_theta = wrk_theta; s.wrk_grad = wrk_grad; s.wrk_logp = wrk_logp; s.p = p; s.H0 = H0;
     s.gl = gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
     s.eps = d_eps; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
@@ -257,11 +264,12 @@ void prof_end(hmc_ctx* x, int id, cudaStream_t st, const std::string& name, doub
   r.bytes = bytes;
 }
 
-void launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag) {
+void launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag,
+                 const PreSplit* pre = nullptr) {
   const int id = prof_begin(x, st);
-  const bool tc = x->tc.accepts(a, akm, bkm);
+  bool tc = x->tc.accepts(a, akm, bkm, pre);
+  if (tc) tc = x->tc.launch(a, akm, bkm, st, pre);
   if (tc) {
-    x->tc.launch(a, akm, bkm, st);
     x->launches++;
   } else {
     launch_gemm_simt(x, a, akm, bkm, st);
@@ -293,7 +301,9 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
   a.epi = EPI_FWD; a.act = L.act;
   if (L.bias) { a.bias = x->Wd + L.b_off; a.s_bias = x->P; }
   if (L.act == ACT_SIN) { a.D = L.D; a.ldd = L.n_out; a.sD = L.rows * L.n_out; }
-  launch_gemm(x, a, true, true, st, "fwd");
+  PreSplit pre;
+  if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo + L.q_off; pre.ld = L.n_in; pre.stride = x->Ptc; }
+  launch_gemm(x, a, true, true, st, "fwd", L.tc_w ? &pre : nullptr);
 }
 
 // backward through layers i = top .. l_min of a net; G of layer `top` is in N.G[cur]
@@ -304,14 +314,37 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
     int64_t s_in;
     const float* in = layer_input(x, N, i, &s_in);
     if (L.any_active) {
-      GemmArgs a = gemm_base(L.n_out, L.n_in + (L.bias ? 1 : 0), (int)L.rows, x->C);
+      GemmArgs a = gemm_base(L.n_out, L.n_in, (int)L.rows, x->C);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
       a.B = in; a.ldb = L.n_in; a.sB = s_in;
-      a.ones_col = L.bias ? L.n_in : -1;
       a.epi = EPI_WGRAD;
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
-      launch_gemm(x, a, false, false, st, "wgrad");
+      const int id = prof_begin(x, st);
+      bool tc = x->tc.accepts(a, false, false);
+      if (tc) tc = x->tc.launch(a, false, false, st);
+      if (tc) {
+        x->launches++;
+        x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
+        prof_end(x, id, st, "tc_wgrad", 2.0 * a.M * a.N * (double)a.K * a.batch,
+                 4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
+        if (L.bias_active) {  // bias gradient = column sums of G (fixed-order two-pass)
+          const int id2 = prof_begin(x, st);
+          const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
+          k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
+                                                           x->colred, chunks);
+          k_colred_p2<<<x->C, 256, 0, st>>>(x->colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
+                                            x->k);
+          x->launches += 2;
+          prof_end(x, id2, st, "bias_grad", 1.0 * x->C * L.rows * L.n_out, 4.0 * x->C * L.rows * L.n_out);
+        }
+      } else {
+        if (L.bias) { a.N += 1; a.ones_col = L.n_in; }
+        launch_gemm_simt(x, a, false, false, st);
+        x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
+        prof_end(x, id, st, "simt_wgrad", 2.0 * a.M * a.N * (double)a.K * a.batch,
+                 4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
+      }
     }
     if (i > N.l_min) {
       const LayerInfo& Pv = x->layers[N.layers[i - 1]];
@@ -321,7 +354,9 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.C = N.G[cur ^ 1]; a.ldc = L.n_in; a.sC = L.rows * L.n_in;
       a.epi = EPI_DACT; a.act = Pv.act;
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
-      launch_gemm(x, a, true, false, st, "dgrad");
+      PreSplit pre;
+      if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo + L.q_off; pre.ld = L.n_in; pre.stride = x->Ptc; }
+      launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr);
       cur ^= 1;
     }
   }
@@ -457,7 +492,7 @@ void build_grad_graph(hmc_ctx* x, std::string& err) {
   const int64_t l0 = x->launches;
   x->prof_armed = false;
   try {
-    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->wrk_theta, x->d_idx, x->Wd, x->k, x->P, x->C);
+    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
     x->launches++;
     enqueue_body(x, x->st);
     x->per_body = x->launches - l0 - 1;
@@ -652,7 +687,31 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (int64_t t = L.w_off; t < L.w_off + (int64_t)L.n_in * L.n_out && !L.any_active; ++t) L.any_active |= slot[t] >= 0;
     if (L.bias) for (int t = 0; t < L.n_out && !L.any_active; ++t) L.any_active |= slot[L.b_off + t] >= 0;
   }
+  for (auto& L : x->layers)
+    if (L.bias)
+      for (int t = 0; t < L.n_out && !L.bias_active; ++t) L.bias_active |= slot[L.b_off + t] >= 0;
   if (x->has_b0) x->b0_slot = slot[x->b0_off];
+  // ---- tensor-core engine: which layers keep tf32 hi/lo weight planes ----
+  x->tc.init();
+  std::vector<int64_t> tcpos((size_t)x->k, -1);
+  if (x->tc.enabled) {
+    for (int ni = 0; ni < x->n_nets; ++ni) {
+      NetInfo& N = x->nets[ni];
+      for (int i = 0; i < (int)N.layers.size(); ++i) {
+        LayerInfo& L = x->layers[N.layers[i]];
+        const bool mlp_out = (x->kind == HMC_MLP && i == (int)N.layers.size() - 1);
+        if (mlp_out || L.n_in % 4 || L.n_out % 4 || L.n_in < 32 || L.n_out < 32) continue;
+        L.tc_w = true;
+        L.q_off = x->Ptc;
+        x->Ptc += (int64_t)L.n_in * L.n_out;
+      }
+    }
+    x->Ptc = (x->Ptc + 3) / 4 * 4;
+    for (int64_t j = 0; j < x->k; ++j)
+      for (auto& L : x->layers)
+        if (L.tc_w && h_idx[j] >= L.w_off && h_idx[j] < L.w_off + (int64_t)L.n_in * L.n_out)
+          tcpos[j] = L.q_off + (h_idx[j] - L.w_off);
+  }
   for (int ni = 0; ni < x->n_nets; ++ni) {
     NetInfo& N = x->nets[ni];
     for (int i = 0; i < (int)N.layers.size(); ++i)
@@ -670,6 +729,17 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   CK(cudaMemcpy(x->d_chain, h_ch.data(), C * 4, cudaMemcpyHostToDevice));
   if (!h_im.empty()) CK(cudaMemcpy(x->d_inv_mass, h_im.data(), x->k * 4, cudaMemcpyHostToDevice));
   for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
+  if (x->Ptc > 0) {
+    x->Whi = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    x->d_tcpos = dalloc<int64_t>(x, x->k, err);
+    CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 8, cudaMemcpyHostToDevice));
+    for (auto& L : x->layers)
+      if (L.tc_w)
+        k_split_layer<<<148 * 4, 256>>>(x->Wd, x->P, L.w_off, (int64_t)L.n_in * L.n_out, x->Whi, x->Wlo, x->Ptc,
+                                         L.q_off, C);
+    CK(cudaGetLastError());
+  }
   const size_t Ck = (size_t)C * x->k;
   x->cur_theta = dalloc<float>(x, Ck, err);
   x->cur_grad = dalloc<float>(x, Ck, err);
@@ -693,9 +763,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->nets[0].input = x->d_x;
     x->n_part = (int)((x->n + 63) / 64);
     x->R = dalloc<float>(x, (size_t)C * x->n, err);
-    const LayerInfo& O = x->layers[x->nets[0].layers.back()];
     x->colred_chunks = (int)((x->n + COLRED_CH - 1) / COLRED_CH);
-    x->colred = dalloc<float>(x, (size_t)C * x->colred_chunks * (O.n_in + 1), err);
   } else {
     x->d_u = dalloc<float>(x, hu.size(), err);
     x->d_q = dalloc<float>(x, hq.size(), err);
@@ -709,11 +777,19 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     const int p = x->layers[x->nets[0].layers.back()].n_out;
     GemmArgs probe = gemm_base((int)x->n_c, (int)x->n_x, p, C);
     probe.epi = EPI_RESID;
-    x->n_part = x->tc.n_tiles(probe, true, true);
-    if (x->n_part <= 0) {
-      const int bm = pick_bm((int)x->n_c, (int)x->n_x);
-      x->n_part = (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm));
+    probe.lda = p; probe.sA = x->n_c * p; probe.ldb = p; probe.sB = x->n_x * p;
+    const int bm = pick_bm((int)x->n_c, (int)x->n_x);
+    // partial slots: max over both engines (unused slots stay zero)
+    x->n_part = std::max(x->tc.n_tiles(probe, true, true),
+                         (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
+  }
+  {  // two-pass column-reduction scratch: max over nets of chunks x (width + 1)
+    size_t cap = 0;
+    for (int ni = 0; ni < x->n_nets; ++ni) {
+      const size_t chunks = (size_t)((x->nets[ni].rows + COLRED_CH - 1) / COLRED_CH);
+      cap = std::max(cap, chunks * (size_t)(x->nets[ni].max_w + 1));
     }
+    x->colred = dalloc<float>(x, (size_t)C * cap, err);
   }
   x->part_sq = dalloc<double>(x, (size_t)C * x->n_part, err);
   x->part_r = dalloc<double>(x, (size_t)C * x->n_part, err);
@@ -952,6 +1028,35 @@ int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream) {
 }
 
 const char* hmc_engine_info(const hmc_ctx* ctx) { return ctx ? ctx->engine.c_str() : ""; }
+
+int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M, int32_t N, int32_t K,
+                   int32_t batch, const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB,
+                   float* C, int64_t ldc, int64_t sC, void* stream) {
+  static TcPlanner tcp;
+  static bool init = false;
+  if (!init) {
+    tcp.init();
+    init = true;
+  }
+  GemmArgs a = gemm_base(M, N, K, batch);
+  a.A = A; a.lda = lda; a.sA = sA; a.B = B; a.ldb = ldb; a.sB = sB; a.C = C; a.ldc = ldc; a.sC = sC;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (engine == 1) {
+    if (!tcp.accepts(a, a_kmajor != 0, b_kmajor != 0) || !tcp.launch(a, a_kmajor != 0, b_kmajor != 0, st)) {
+      g_err = "tcgen05 engine does not take this GEMM";
+      return HMC_E_CONFIG;
+    }
+  } else {
+    hmc_ctx dummy;
+    launch_gemm_simt(&dummy, a, a_kmajor != 0, b_kmajor != 0, st);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return HMC_E_CUDA;
+  }
+  return HMC_OK;
+}
 
 int hmc_profile(hmc_ctx* ctx, int32_t enable) {
   API_BEGIN(ctx)

@@ -24,6 +24,9 @@ struct KState {
   const float* inv_mass;       // nullptr = identity
   const uint32_t* chain_ids;
   float* Wd;                   // [C x P] dense per-chain parameters (frozen mu + active theta)
+  float* Whi; float* Wlo;      // [C x Ptc] tf32 hi / lo planes of the tensor-core layers' weights
+  const int64_t* tcpos;        // [k] position of active entry j in the planes, -1 if none
+  int64_t Ptc;
   float* cur_theta; float* cur_grad; double* cur_logp;   // chain state (the cache)
   float* wrk_theta; float* wrk_grad; double* wrk_logp;   // trajectory working state
   float* p; double* H0;
@@ -38,14 +41,40 @@ struct KState {
 
 constexpr int KT = 256;  // threads of the per-chain state kernels
 
+// theta_j of chain c -> dense parameters (and the tf32 hi/lo planes of tensor-core layers)
+__device__ __forceinline__ void put_param(const KState& s, int64_t c, int64_t j, float th) {
+  s.Wd[c * s.P + s.idx[j]] = th;
+  if (s.tcpos) {
+    const int64_t q = s.tcpos[j];
+    if (q >= 0) {
+      const float h = tf32_hi(th);
+      s.Whi[c * s.Ptc + q] = h;
+      s.Wlo[c * s.Ptc + q] = th - h;
+    }
+  }
+}
+
 // ---- scatter theta_s into the dense per-chain parameter vector (Theta_~s = mu_~s) --
-__global__ void k_scatter(const float* __restrict__ theta, const int32_t* __restrict__ idx,
-                          float* __restrict__ Wd, int64_t k, int64_t P, int C) {
-  const int64_t total = (int64_t)C * k;
+__global__ void k_scatter(KState s, const float* __restrict__ theta) {
+  const int64_t total = (int64_t)s.C * s.k;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / k, j = t - c * k;
-    Wd[c * P + idx[j]] = theta[t];
+    const int64_t c = t / s.k, j = t - c * s.k;
+    put_param(s, c, j, theta[t]);
+  }
+}
+
+// tf32 hi/lo planes of one layer's weights for every chain, from the dense parameters
+__global__ void k_split_layer(const float* __restrict__ Wd, int64_t P, int64_t w_off, int64_t n,
+                              float* __restrict__ Whi, float* __restrict__ Wlo, int64_t Ptc, int64_t q_off, int C) {
+  const int64_t total = (int64_t)C * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / n, i = t - c * n;
+    const float w = Wd[c * P + w_off + i];
+    const float h = tf32_hi(w);
+    Whi[c * Ptc + q_off + i] = h;
+    Wlo[c * Ptc + q_off + i] = w - h;
   }
 }
 
@@ -107,14 +136,15 @@ __global__ void k_colred_p1(const float* __restrict__ R, const float* __restrict
                             int64_t rows, int n_in, float* __restrict__ part, int n_chunks) {
   const int c = blockIdx.y, ch = blockIdx.x;
   const float* Xc = X + (int64_t)c * sX;
-  const float* Rc = R + (int64_t)c * rows;
+  const float* Rc = R ? R + (int64_t)c * rows : nullptr;
   const int64_t n0 = (int64_t)ch * COLRED_CH;
   const int64_t n1 = min(rows, n0 + COLRED_CH);
   for (int j = threadIdx.x; j <= n_in; j += blockDim.x) {
     float s = 0.f;
     if (j < n_in) {
-      for (int64_t n = n0; n < n1; ++n) s = fmaf(Rc[n], Xc[n * n_in + j], s);
-    } else {
+      if (R) for (int64_t n = n0; n < n1; ++n) s = fmaf(Rc[n], Xc[n * n_in + j], s);
+      else for (int64_t n = n0; n < n1; ++n) s += Xc[n * n_in + j];
+    } else if (R) {
       for (int64_t n = n0; n < n1; ++n) s += Rc[n];
     }
     part[((int64_t)c * n_chunks + ch) * (n_in + 1) + j] = s;
@@ -178,7 +208,7 @@ __global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
       s.p[t] = p;
       th = fmaf(fe * im, p, th);
       s.wrk_theta[t] = th;
-      s.Wd[(int64_t)c * s.P + s.idx[j]] = th;
+      put_param(s, c, j, th);
     } else if (mode == 2) {
       s.p[t] = fmaf(fh, g, s.p[t]);
     }
@@ -218,7 +248,7 @@ __global__ void __launch_bounds__(KT) k_traj_begin(KState s, int L0) {
       } else {
         p = fmaf(fh, s.cur_grad[t], p);
         th = fmaf(fe * im, p, th);
-        s.Wd[(int64_t)c * s.P + s.idx[j]] = th;
+        put_param(s, c, j, th);
       }
       s.p[t] = p;
       s.wrk_theta[t] = th;

@@ -1,13 +1,582 @@
-// tcgen05 3xTF32 GEMM engine (placeholder until the tensor-core path lands): accepts nothing,
-// so every GEMM runs on the SIMT engine.
+// tcgen05 3xTF32 GEMM engine for the wide layers (libhmc, sm_100a only).
+//
+// C[b] = A[b] . B[b] with FP32 accuracy from three TF32 tensor-core products per K step:
+//   A = Ah + Al, B = Bh + Bl, Ah = rna_tf32(A), Al = A - Ah (exact in fp32),
+//   C ~= Al.Bh + Ah.Bl + Ah.Bh accumulated in fp32 in TMEM (SURVEY Q25:
+//   1xTF32 misses the 1e-5 gradient tolerance, 3xTF32 meets it).
+// Structure (persistent, one CTA per SM, 256 threads):
+//   warp 0    : TMA producer  - fp32 tiles (128B-swizzled) of A and B into a 2-3 stage ring
+//   warp 1    : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8) x 3 per K step
+//   warps 2-3 : converters    - split the landed fp32 tiles into hi (in place) / lo planes
+//   warps 4-7 : epilogue      - tcgen05.ld the accumulator (one TMEM lane = one row per thread),
+//               apply the fused epilogue of gemm_simt.cuh (bias+act / act' / residual^2 /
+//               masked weight-gradient compaction) and store
+// The accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
+// overlaps the MMAs of tile i+1.  Operand layouts: K-major or MN-major (TF32 supports both in
+// SMEM descriptors); weights arrive pre-split (hi/lo planes written by the scatter kernel).
 #pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
 #include "gemm_simt.cuh"
 
 namespace hmc {
-struct TcPlanner {
-  bool accepts(const GemmArgs&, bool, bool) const { return false; }
-  void launch(const GemmArgs&, bool, bool, cudaStream_t) const {}
-  int n_tiles(const GemmArgs&, bool, bool) const { return -1; }
-  const char* describe() const { return "simt"; }
+namespace tc {
+
+constexpr int BM = 128;   // UMMA M (cta_group::1)
+constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
+constexpr int NT = 256;   // threads
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = (BN == 256) ? 2 : 3;
+  static constexpr int A_BYTES = BM * BK * 4;           // 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;           // 32 / 16 KB
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;              // double-buffered accumulator
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+// ---------------------------------------------------------------- PTX wrappers (sm_100a) ---
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* holder, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(holder)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns: thread (lane i of the warp) gets row (lane base+i),
+// columns [col, col+32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%"
+      "30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// SMEM matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+//  K-major : rows of 128 B (32 fp32 along K), 8-row atoms at SBO = 1024 B, LBO unused (1).
+//  MN-major: 128 B = 32 fp32 along M/N, 8 K-rows per atom (SBO = 1024 B between 8-row K groups),
+//            32-element M/N blocks at LBO bytes.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                          uint32_t layout = 2) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;            // version (sm_100)
+  d |= (uint64_t)(layout & 7) << 61; // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// MN-major 32-bit operands: CUTLASS allows only the 128B swizzle with 32-byte atoms
+// (SWIZZLE_128B_BASE32B, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).  Descriptor parameters are
+// kernel arguments so the encoding is verified on the device (tests/test_gpu_engine.py).
+struct MnDesc {
+  uint32_t lbo = 4096, sbo = 512, layout = 1, kstep = 1024;
+};
+
+// Instruction descriptor for kind::tf32 with fp32 accumulation.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4)                      // D format f32
+         | (2u << 7) | (2u << 10)       // A, B format tf32
+         | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------------------- kernel ---
+// A_MN: A stored M-major (A(m,k) = A[k*lda + m]);  B_MN: B stored N-major (B(k,n) = B[k*ldb + n]);
+// B_PRE: B arrives as pre-split hi/lo planes (tensor maps mB / mB2).
+template <int BN, bool A_MN, bool B_MN, bool B_PRE>
+__global__ void __launch_bounds__(NT, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+                   const __grid_constant__ CUtensorMap mB2, GemmArgs a, MnDesc mn) {
+  using C_ = Cfg<BN>;
+  constexpr int S = C_::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = (uint64_t*)(smem + S * C_::STAGE_BYTES);
+  uint64_t* full_raw = bar;           // [S]  TMA -> converters
+  uint64_t* full_op = bar + S;        // [S]  converters -> MMA
+  uint64_t* empty = bar + 2 * S;      // [S]  MMA -> TMA
+  uint64_t* tfull = bar + 3 * S;      // [2]  MMA -> epilogue
+  uint64_t* tempty = bar + 3 * S + 2; // [2]  epilogue -> MMA
+  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 4);
+  double* red = (double*)(bar + 3 * S + 6);  // [8] epilogue reductions
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
+  const int tiles_per_b = n_mt * n_nt;
+  const int total = tiles_per_b * a.batch;
+  const int nk = (a.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_raw[s], 1);
+      mbar_init(&full_op[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tma_prefetch(&mA);
+    tma_prefetch(&mB);
+    if (B_PRE) tma_prefetch(&mB2);
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, C_::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ================================ TMA producer ================================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t bytes = C_::A_BYTES + (B_PRE ? 2 : 1) * C_::B_BYTES;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
+        const int mt = rem / n_nt, nt = rem - mt * n_nt;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * C_::STAGE_BYTES;
+          uint8_t* sAh = st;
+          uint8_t* sBh = st + 2 * C_::A_BYTES;
+          uint8_t* sBl = sBh + C_::B_BYTES;
+          mbar_expect_tx(&full_raw[s], bytes);
+          if (A_MN) tma_load4(sAh, &mA, &full_raw[s], 0, kb * BK, mt * (BM / 32), b);
+          else tma_load3(sAh, &mA, &full_raw[s], kb * BK, mt * BM, b);
+          if (B_MN) {
+            tma_load4(sBh, &mB, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
+            if (B_PRE) tma_load4(sBl, &mB2, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
+          } else {
+            tma_load3(sBh, &mB, &full_raw[s], kb * BK, nt * BN, b);
+            if (B_PRE) tma_load3(sBl, &mB2, &full_raw[s], kb * BK, nt * BN, b);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================ MMA issuer ==================================
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_tf32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int j = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+        const int accb = j & 1;
+        mbar_wait(&tempty[accb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + accb * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_op[s], ph);
+          tc_fence_after();
+          const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
+          const uint32_t aH = st, aL = st + C_::A_BYTES;
+          const uint32_t bH = st + 2 * C_::A_BYTES, bL = bH + C_::B_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // K offset of this K=8 slice inside the stage
+            const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
+            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
+            const uint32_t a_lbo = A_MN ? mn.lbo : 16, b_lbo = B_MN ? mn.lbo : 16;
+            const uint32_t a_sbo = A_MN ? mn.sbo : 1024, b_sbo = B_MN ? mn.sbo : 1024;
+            const uint32_t a_lay = A_MN ? mn.layout : 2, b_lay = B_MN ? mn.layout : 2;
+            const uint64_t dAh = sdesc(aH + ao, a_lbo, a_sbo, a_lay), dAl = sdesc(aL + ao, a_lbo, a_sbo, a_lay);
+            const uint64_t dBh = sdesc(bH + bo, b_lbo, b_sbo, b_lay), dBl = sdesc(bL + bo, b_lbo, b_sbo, b_lay);
+            const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+            mma_tf32(dcol, dAl, dBh, IDESC, first);
+            mma_tf32(dcol, dAh, dBl, IDESC, 1u);
+            mma_tf32(dcol, dAh, dBh, IDESC, 1u);
+          }
+          mma_commit(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        mma_commit(&tfull[accb]);
+      }
+    }
+  } else if (warp < 4) {
+    // ================================ converters ==================================
+    const int ct = threadIdx.x - 64;  // 0..63
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full_raw[s], ph);
+        uint8_t* st = smem + s * C_::STAGE_BYTES;
+        float4* ah = (float4*)st;
+        float4* al = (float4*)(st + C_::A_BYTES);
+#pragma unroll 4
+        for (int i = ct; i < C_::A_BYTES / 16; i += 64) {
+          const float4 x = ah[i];
+          float4 h, l;
+          h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          ah[i] = h;
+          al[i] = l;
+        }
+        if (!B_PRE) {
+          float4* bh = (float4*)(st + 2 * C_::A_BYTES);
+          float4* bl = (float4*)(st + 2 * C_::A_BYTES + C_::B_BYTES);
+#pragma unroll 4
+          for (int i = ct; i < C_::B_BYTES / 16; i += 64) {
+            const float4 x = bh[i];
+            float4 h, l;
+            h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+            l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+            bh[i] = h;
+            bl[i] = l;
+          }
+        }
+        fence_proxy_async();
+        mbar_arrive(&full_op[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // ================================ epilogue ====================================
+    const int e = threadIdx.x - 128;      // 0..127 = TMEM lane = tile row
+    const int ew = e >> 5;                // epilogue warp -> TMEM lanes [32 ew, 32 ew + 32)
+    int j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
+      const int mt = rem / n_nt, nt = rem - mt * n_nt;
+      const int accb = j & 1;
+      mbar_wait(&tfull[accb], (j >> 1) & 1);
+      tc_fence_after();
+      const int m = mt * BM + e;
+      const bool mrow = m < a.M;
+      double psq = 0.0, pr = 0.0;
+      const float b0v = (a.epi == EPI_RESID && a.b0) ? a.b0[(int64_t)b * a.s_b0] : 0.f;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * ew) << 16) + accb * BN + c0, v);
+        const int n0 = nt * BN + c0;
+        if (!mrow || n0 >= a.N) continue;
+        const int nmax = min(32, a.N - n0);
+        switch (a.epi) {
+          case EPI_FWD: {
+            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
+            const float* bias = a.bias ? a.bias + (int64_t)b * a.s_bias + n0 : nullptr;
+            float* D = a.D ? a.D + (int64_t)b * a.sD + (int64_t)m * a.ldd + n0 : nullptr;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < nmax) {
+                float z = v[i] + (bias ? bias[i] : 0.f);
+                if (D) D[i] = cosf(z);
+                dst[i] = act_fwd(a.act, z);
+              }
+            }
+          } break;
+          case EPI_DACT: {
+            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
+            const float* ds = a.dsrc ? a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0 : nullptr;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < nmax) {
+                float z = v[i];
+                if (a.act == ACT_TANH) { const float tt = ds[i]; z *= (1.f - tt * tt); }
+                else if (a.act == ACT_SIN) z *= ds[i];
+                dst[i] = z;
+              }
+            }
+          } break;
+          case EPI_WGRAD: {
+            const int32_t* sw = a.slot_w + (int64_t)m * a.n_in + n0;
+            float* gl = a.gl + (int64_t)b * a.k;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < nmax) {
+                const int sl = sw[i];
+                if (sl >= 0) gl[sl] = v[i];
+              }
+            }
+          } break;
+          case EPI_RESID: {
+            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
+            const float* V = a.V + (int64_t)m * a.ldv + n0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < nmax) {
+                const float o = v[i] + b0v;
+                const float r = V[i] - o;
+                const float R = (float)((double)r * a.inv_s2);
+                dst[i] = R;
+                psq += (double)r * (double)r;
+                pr += (double)R;
+              }
+            }
+          } break;
+          default: {
+            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nmax) dst[i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[accb]);
+      if (a.epi == EPI_RESID) {
+        // deterministic 128-thread reduction: warp shuffles, then fixed-order sum of 4 warps
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          psq += __shfl_down_sync(0xffffffffu, psq, o);
+          pr += __shfl_down_sync(0xffffffffu, pr, o);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (lane == 0) { red[ew] = psq; red[4 + ew] = pr; }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (e == 0) {
+          a.part_sq[(int64_t)b * a.n_part + rem] = ((red[0] + red[1]) + red[2]) + red[3];
+          a.part_r[(int64_t)b * a.n_part + rem] = ((red[4] + red[5]) + red[6]) + red[7];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, C_::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------------- host side ---
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace tc
+
+// Pre-split operand description (hi / lo planes of the weights) attached to a GemmArgs.
+struct PreSplit {
+  const float* hi = nullptr;
+  const float* lo = nullptr;
+  int64_t ld = 0, stride = 0;
+};
+
+struct TcPlanner {
+  bool enabled = false;
+  int num_sms = 148;
+  tc::EncodeTiledFn encode = nullptr;
+  tc::MnDesc mn;
+  CUtensorMapSwizzle mn_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+
+  void init() {
+    enabled = false;
+    const char* eng = getenv("HMC_ENGINE");
+    if (eng && strcmp(eng, "simt") == 0) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return;
+    if (p.major != 10 || p.minor != 0) return;  // sm_100a binary only
+    num_sms = p.multiProcessorCount;
+    if (const char* v = getenv("HMC_MN_LBO")) mn.lbo = (uint32_t)atoi(v);
+    if (const char* v = getenv("HMC_MN_SBO")) mn.sbo = (uint32_t)atoi(v);
+    if (const char* v = getenv("HMC_MN_LAYOUT")) mn.layout = (uint32_t)atoi(v);
+    if (const char* v = getenv("HMC_MN_KSTEP")) mn.kstep = (uint32_t)atoi(v);
+    if (const char* v = getenv("HMC_MN_TMA")) mn_swizzle = atoi(v) == 32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                                        : CU_TENSOR_MAP_SWIZZLE_128B;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
+    encode = (tc::EncodeTiledFn)fn;
+    static bool attr_done = false;
+    if (!attr_done) {
+      set_attrs();
+      attr_done = true;
+    }
+    enabled = true;
+  }
+
+  static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+  // Shapes / layouts the tensor-core engine takes (everything else runs on the SIMT engine).
+  bool accepts(const GemmArgs& a, bool akm, bool bkm, const PreSplit* pre = nullptr) const {
+    if (!enabled) return false;
+    if (a.ones_col >= 0) return false;
+    if (a.M < 64 || a.N < 32 || a.K < 32) return false;
+    if (a.batch > 65535) return false;
+    const bool amn = !akm, bmn = !bkm;
+    if ((a.lda % 4) || (a.sA % 4) || !al16(a.A) || (a.sA == 0 && a.batch > 1)) return false;
+    if (amn && (a.M % 32)) return false;
+    if (pre) {
+      if (!pre->hi || (pre->ld % 4) || (pre->stride % 4) || !al16(pre->hi) || !al16(pre->lo)) return false;
+    } else {
+      if ((a.ldb % 4) || (a.sB % 4) || !al16(a.B) || (a.sB == 0 && a.batch > 1)) return false;
+    }
+    if (bmn && (a.N % 32)) return false;
+    return true;
+  }
+
+  static int bn_for(int N) { return N <= 128 ? 128 : 256; }
+
+  int n_tiles(const GemmArgs& a, bool akm, bool bkm) const {
+    if (!accepts(a, akm, bkm)) return -1;
+    const int bn = bn_for(a.N);
+    return ((a.M + tc::BM - 1) / tc::BM) * ((a.N + bn - 1) / bn);
+  }
+
+  const char* describe() const { return enabled ? "tcgen05-3xtf32+simt" : "simt"; }
+
+  // K-major operand X(row, k) = X[row*ld + k] per batch: dims (K, rows, batch), box (32, rows_box, 1)
+  bool map_kmajor(CUtensorMap* m, const float* base, int64_t rows, int64_t K, int64_t ld, int64_t bstride,
+                  int batch, int box_rows) const {
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(bstride ? bstride : rows * ld) * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  // MN-major operand X(k, j) = X[k*ld + j] per batch: dims (32, K, MN/32, batch), box (32, 32, box_mn/32, 1)
+  bool map_mnmajor(CUtensorMap* m, const float* base, int64_t K, int64_t MN, int64_t ld, int64_t bstride,
+                   int batch, int box_mn) const {
+    cuuint64_t dims[4] = {32, (cuuint64_t)K, (cuuint64_t)(MN / 32), (cuuint64_t)batch};
+    cuuint64_t strides[3] = {(cuuint64_t)ld * 4, 128, (cuuint64_t)(bstride ? bstride : K * ld) * 4};
+    cuuint32_t box[4] = {32, 32, (cuuint32_t)(box_mn / 32), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, mn_swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
+  template <int BN, bool AMN, bool BMN, bool PRE>
+  static void set_attr_one() {
+    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, AMN, BMN, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tc::Cfg<BN>::SMEM);
+  }
+  static void set_attrs() {
+#define SA(BN)                               \
+  set_attr_one<BN, false, false, false>();   \
+  set_attr_one<BN, false, false, true>();    \
+  set_attr_one<BN, false, true, false>();    \
+  set_attr_one<BN, false, true, true>();     \
+  set_attr_one<BN, true, true, false>();     \
+  set_attr_one<BN, true, false, false>();
+    SA(128)
+    SA(256)
+#undef SA
+  }
+
+  // Returns false if a tensor map could not be encoded (caller falls back to SIMT).
+  bool launch(const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const PreSplit* pre = nullptr) const {
+    const int bn = bn_for(a.N);
+    const bool amn = !akm, bmn = !bkm;
+    CUtensorMap mA, mB, mB2;
+    memset(&mB2, 0, sizeof(mB2));
+    bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM)
+                  : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
+    if (pre) {
+      ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, bn)
+                      : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, bn));
+      ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, bn)
+                      : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, bn));
+    } else {
+      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, bn)
+                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, bn));
+      mB2 = mB;
+    }
+    if (!ok) return false;
+    const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + bn - 1) / bn) * a.batch;
+    const int grid = tiles < num_sms ? tiles : num_sms;
+    const bool p = pre != nullptr;
+#define TL(BN, AMN, BMN, PRE) \
+  tc::tc_gemm_kernel<BN, AMN, BMN, PRE><<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, a, mn)
+#define TLB(BN)                                      \
+  if (!amn && !bmn && !p) TL(BN, false, false, false); \
+  else if (!amn && !bmn && p) TL(BN, false, false, true); \
+  else if (!amn && bmn && !p) TL(BN, false, true, false); \
+  else if (!amn && bmn && p) TL(BN, false, true, true); \
+  else if (amn && bmn && !p) TL(BN, true, true, false); \
+  else if (amn && !bmn && !p) TL(BN, true, false, false); \
+  else return false;
+    if (bn == 128) { TLB(128) } else { TLB(256) }
+#undef TLB
+#undef TL
+    return true;
+  }
+};
+
 }  // namespace hmc

@@ -1,0 +1,101 @@
+"""World-size-2 gloo tests (CPU) of the data-parallel host logic: row sharding, NCCL-id
+broadcast, and the reduction algebra libhmc relies on in DATA mode (sum of per-shard likelihood
+gradients, prior added once after the all-reduce == full-batch gradient)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from hmcdata import ArchSpec, NetSpec, make_tiny_problem
+from paper_2507_14652_b200 import dist as pdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, q):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import hmc as ohmc
+    from oracle import network as onet
+    if kind == "mlp":
+        arch = ArchSpec("mlp", (NetSpec.plain((2, 7, 5, 1)),))
+        prob = make_tiny_problem(arch, n=37, active_frac=0.5, seed=3, noise=0.4)
+    else:
+        arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")),
+                        has_b0=True)
+        prob = make_tiny_problem(arch, n_c=11, n_x=9, active_frac=0.6, seed=4, noise=0.4)
+    shard, n_global = pdist.shard_rows(prob, rank, world)
+    th = prob.frozen[prob.idx].astype(np.float64) + 0.01
+    t = ohmc.Target(shard)
+    full = t.assemble(th)
+    ll, g_full, _ = onet.loglik_grad(arch, full, t.data, t.sigma)
+    buf = torch.tensor(np.concatenate([g_full[prob.idx], [ll]]), dtype=torch.float64)
+    dist.all_reduce(buf)                      # the DATA-mode reduction: likelihood sums only
+    sp2 = prob.prior_sigma ** 2
+    g = buf[:-1].numpy() - th / sp2           # prior added once, after the reduction
+    lp = buf[-1].item() - np.dot(th, th) / (2 * sp2)
+    # NCCL id broadcast path (any 128-byte payload)
+    nid = pdist.broadcast_nccl_id(lambda: bytes(range(128)))
+    q.put((rank, lp, g, n_global, nid))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["mlp", "deeponet"])
+def test_data_mode_reduction_matches_full_batch(kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    from oracle import hmc as ohmc
+    if kind == "mlp":
+        arch = ArchSpec("mlp", (NetSpec.plain((2, 7, 5, 1)),))
+        prob = make_tiny_problem(arch, n=37, active_frac=0.5, seed=3, noise=0.4)
+        N = 37
+    else:
+        arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")),
+                        has_b0=True)
+        prob = make_tiny_problem(arch, n_c=11, n_x=9, active_frac=0.6, seed=4, noise=0.4)
+        N = 99
+    th = prob.frozen[prob.idx].astype(np.float64) + 0.01
+    lp_ref, g_ref = ohmc.Target(prob).logp_grad(th)
+    for rank, lp, g, n_global, nid in res:
+        assert n_global == N
+        assert nid == bytes(range(128))
+        assert lp == pytest.approx(lp_ref, rel=1e-12)
+        np.testing.assert_allclose(g, g_ref, rtol=1e-11, atol=1e-11)
+    # both ranks hold bitwise-identical reduced values (MH decisions agree without a broadcast)
+    np.testing.assert_array_equal(res[0][2], res[1][2])
+
+
+def test_row_blocks_partition_rows():
+    for n in (1, 7, 37, 1024):
+        for w in (1, 2, 3, 8):
+            blocks = [pdist.row_block(n, r, w) for r in range(w)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(blocks[i][1] == blocks[i + 1][0] for i in range(w - 1))
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_chain_ids_are_global_and_disjoint():
+    ids = [set(pdist.chain_ids(r, 64).tolist()) for r in range(8)]
+    assert set.union(*ids) == set(range(512))
+    assert sum(len(s) for s in ids) == 512

@@ -76,6 +76,40 @@ def test_grad_tiny(name):
         assert_grad_close(lp[ci], g[ci], lr, gr, f"{name} chain {ci}")
 
 
+@pytest.mark.parametrize("name", ["mlp_ragged", "deeponet_ragged"])
+def test_grad_simt_engine_forced(name, monkeypatch):
+    """The SIMT engine alone (HMC_ENGINE=simt) meets the same tolerances."""
+    monkeypatch.setenv("HMC_ENGINE", "simt")
+    arch, kw = TINY[name]
+    prob = make_tiny_problem(arch, n_chains=2, seed=11, noise=0.3, **kw)
+    th = jittered_states(prob, 2)
+    with _ctx(prob) as c:
+        from paper_2507_14652_b200 import abi
+        assert abi.hmc_engine_info(c.ctx) == "simt"
+        lp, g = gpu_grad(c, th)
+    t = ohmc.Target(prob)
+    for ci in range(2):
+        lr, gr = t.logp_grad(th[ci])
+        assert_grad_close(lp[ci], g[ci], lr, gr, name)
+
+
+def test_grad_cfg5_engines_agree(monkeypatch):
+    """cfg5 gradient: tcgen05 engine vs SIMT engine vs oracle (chain 0)."""
+    prob = make_problem("cfg5", n_chains=4)
+    th = jittered_states(prob, 4)
+    with _ctx(prob) as c:
+        from paper_2507_14652_b200 import abi
+        assert "tcgen05" in abi.hmc_engine_info(c.ctx)
+        lp_tc, g_tc = gpu_grad(c, th)
+    monkeypatch.setenv("HMC_ENGINE", "simt")
+    with _ctx(prob) as c:
+        lp_s, g_s = gpu_grad(c, th)
+    t = ohmc.Target(prob)
+    lr, gr = t.logp_grad(th[0])
+    assert_grad_close(lp_tc[0], g_tc[0], lr, gr, "tc")
+    assert_grad_close(lp_s[0], g_s[0], lr, gr, "simt")
+
+
 def test_grad_case1_sine_and_blr():
     case1 = ArchSpec("mlp", (NetSpec((1, 2, 1), ("sin", "identity"), (True, False)),))
     for prob in (make_tiny_problem(case1, n=20, seed=4, noise=0.1), make_problem("blr", n_chains=2)):
