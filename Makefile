@@ -6,9 +6,13 @@ FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-rel
 SRC := paper_2507_14652_b200/csrc/hmc.cu
 DEPS := $(wildcard paper_2507_14652_b200/csrc/*.cuh) include/hmc.h
 LIB := paper_2507_14652_b200/libhmc.so
+# link the NCCL that ships with torch (same soname, newer than the system copy) and find it at run time
+PYTHON ?= python
+NCCL_LIB := $(shell $(PYTHON) -c "import os, nvidia.nccl as m; print(os.path.join(list(m.__path__)[0], 'lib'))" 2>/dev/null)
+NCCL_LINK := $(if $(NCCL_LIB),-L$(NCCL_LIB) -Xlinker -rpath=$(NCCL_LIB) -l:libnccl.so.2,-lnccl)
 
 $(LIB): $(SRC) $(DEPS)
-	$(NVCC) $(FLAGS) -Iinclude -shared -o $@ $(SRC) -lnccl 2> build/ptxas.log || (cat build/ptxas.log; false)
+	$(NVCC) $(FLAGS) -Iinclude -shared -o $@ $(SRC) $(NCCL_LINK) 2> build/ptxas.log || (cat build/ptxas.log; false)
 
 all: $(LIB)
 clean:

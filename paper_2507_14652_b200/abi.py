@@ -70,6 +70,10 @@ def lib():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise RuntimeError(f"{LIB_PATH} is not built; run `make` or __graft_entry__.build()")
+    # libhmc.so needs libnccl.so.2.  Load torch first so its bundled NCCL (the one libtorch_cuda
+    # was built against) is the copy in the process; loading the system NCCL first would leave
+    # torch with unresolved NCCL symbols.
+    import torch  # noqa: F401  (plumbing: device memory, streams, process groups)
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, u32, u64, dbl = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
                                    ctypes.c_uint64, ctypes.c_double)
