@@ -2,18 +2,26 @@
 //
 // C[b] = A[b] . B[b] with FP32 accuracy from three TF32 tensor-core products per K step:
 //   A = Ah + Al, B = Bh + Bl, Ah = rna_tf32(A), Al = A - Ah (exact in fp32),
-//   C ~= Al.Bh + Ah.Bl + Ah.Bh accumulated in fp32 in TMEM (SURVEY Q25:
-//   1xTF32 misses the 1e-5 gradient tolerance, 3xTF32 meets it).
-// Structure (persistent, one CTA per SM, 256 threads):
-//   warp 0    : TMA producer  - fp32 tiles (128B-swizzled) of A and B into a 2-3 stage ring
-//   warp 1    : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8) x 3 per K step
-//   warps 2-3 : converters    - split the landed fp32 tiles into hi (in place) / lo planes
-//   warps 4-7 : epilogue      - tcgen05.ld the accumulator (one TMEM lane = one row per thread),
-//               apply the fused epilogue of gemm_simt.cuh (bias+act / act' / residual^2 /
-//               masked weight-gradient compaction) and store
-// The accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile i
-// overlaps the MMAs of tile i+1.  Operand layouts: K-major or MN-major (TF32 supports both in
-// SMEM descriptors); weights arrive pre-split (hi/lo planes written by the scatter kernel).
+//   C ~= Al.Bh + Ah.Bl + Ah.Bh   (1xTF32 misses the 1e-5 gradient
+//   tolerance, 3xTF32 meets it).
+// Accumulation: the tensor core truncates its fp32 accumulator toward zero after every MMA
+// (measured on B200, scripts/probe_tc_rounding.py: 1 + 1.5*2^-24 -> 1.0), a bias that grows
+// with the number of MMAs per accumulator (1.7e-4 relative at K = 16384).  So every 32-wide K
+// block is accumulated in its own TMEM buffer (small products first, then the big Ah.Bh
+// products: 4 truncations at most relative to the block's partial sum) and the epilogue warps
+// fold the block partials into fp32 registers with round-to-nearest adds.  The chunk buffers
+// are ping-ponged (512 / BN of them) so the MMAs of block j+1 overlap the fold of block j.
+// Structure (persistent, one CTA per SM, 384 threads):
+//   warp 0     : TMA producer  - fp32 tiles (128B-swizzled) of A and B into a STAGES-deep ring
+//   warp 1     : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8) x 12 per K block
+//   warps 2-3  : converters    - split the landed fp32 tiles into hi (in place) / lo planes
+//   warps 4-11 : epilogue      - fold (tcgen05.ld 32x32b) into BN/2 fp32 registers per thread
+//               (warp w: TMEM lane quadrant w%4 = 32 tile rows, column half (w-4)/4), then the
+//               fused epilogue (bias+act / act' / residual^2 / masked weight-gradient
+//               compaction); outputs staged through a 128B-swizzled smem tile per warp and
+//               written with TMA bulk tensor stores (coalesced, OOB-clipped).
+// Operand layouts: K-major or MN-major (TF32 supports both in SMEM descriptors); the weights
+// arrive pre-split (hi/lo planes written by the scatter kernel).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -28,7 +36,9 @@ namespace tc {
 
 constexpr int BM = 128;   // UMMA M (cta_group::1)
 constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
-constexpr int NT = 256;   // threads
+constexpr int NT = 384;   // threads
+constexpr int NEPI = 8;   // epilogue warps
+constexpr int STG = 4096; // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
 template <int BN>
 struct Cfg {
@@ -36,8 +46,9 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;           // 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // 32 / 16 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;              // double-buffered accumulator
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int NBUF = 512 / BN;                 // TMEM K-block accumulators
+  static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
+  static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * STG + 512 /*barriers*/;
 };
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a) ---
@@ -107,23 +118,28 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// 32 lanes x 32 consecutive 32-bit columns: thread (lane i of the warp) gets row (lane base+i),
-// columns [col, col+32).
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
+// 32 lanes x 16 consecutive 32-bit columns: thread (lane i of the warp) gets TMEM lane
+// (lane base + i), columns [col, col + 16).  Caller waits with tmem_wait_ld().
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%"
-      "30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// TMA bulk tensor store smem -> global (3-D map), bulk-group completion.
+__device__ __forceinline__ void tma_store3(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   (uint64_t)m),
+               "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -162,24 +178,41 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_
 }
 
 // ------------------------------------------------------------------------------- kernel ---
+// fp32 x 32 of one tile row (columns n0 .. n0+31) from global memory, zero outside [0, N)
+__device__ __forceinline__ void load_row32(const float* __restrict__ p, int n0, int N, bool vec, float (&v)[32]) {
+  if (vec && n0 + 32 <= N) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p) + q);
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = (n0 + i < N) ? __ldg(p + i) : 0.f;
+  }
+}
+
 // A_MN: A stored M-major (A(m,k) = A[k*lda + m]);  B_MN: B stored N-major (B(k,n) = B[k*ldb + n]);
-// B_PRE: B arrives as pre-split hi/lo planes (tensor maps mB / mB2).
+// B_PRE: B arrives as pre-split hi/lo planes (tensor maps mB / mB2).  mC: 3-D store map of the
+// output (box 32 x 32 x 1, 128B swizzle) for every epilogue except EPI_WGRAD.
 template <int BN, bool A_MN, bool B_MN, bool B_PRE>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-                   const __grid_constant__ CUtensorMap mB2, GemmArgs a, MnDesc mn) {
+                   const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC, GemmArgs a,
+                   MnDesc mn) {
   using C_ = Cfg<BN>;
-  constexpr int S = C_::STAGES;
+  constexpr int S = C_::STAGES, NBUF = C_::NBUF, NC = C_::NC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bar = (uint64_t*)(smem + S * C_::STAGE_BYTES);
-  uint64_t* full_raw = bar;           // [S]  TMA -> converters
-  uint64_t* full_op = bar + S;        // [S]  converters -> MMA
-  uint64_t* empty = bar + 2 * S;      // [S]  MMA -> TMA
-  uint64_t* tfull = bar + 3 * S;      // [2]  MMA -> epilogue
-  uint64_t* tempty = bar + 3 * S + 2; // [2]  epilogue -> MMA
-  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 4);
-  double* red = (double*)(bar + 3 * S + 6);  // [8] epilogue reductions
+  uint8_t* stg_base = smem + S * C_::STAGE_BYTES;
+  uint64_t* bar = (uint64_t*)(stg_base + NEPI * STG);
+  uint64_t* full_raw = bar;               // [S]    TMA -> converters
+  uint64_t* full_op = bar + S;            // [S]    converters -> MMA
+  uint64_t* empty = bar + 2 * S;          // [S]    MMA -> TMA
+  uint64_t* tfull = bar + 3 * S;          // [NBUF] MMA -> epilogue (K-block partial ready)
+  uint64_t* tempty = bar + 3 * S + NBUF;  // [NBUF] epilogue -> MMA (partial folded)
+  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 * NBUF);
+  double* red = (double*)(bar + 3 * S + 2 * NBUF + 1);  // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -193,16 +226,17 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&full_op[s], 64);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], NEPI * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
     tma_prefetch(&mB);
     if (B_PRE) tma_prefetch(&mB2);
+    if (a.epi != EPI_WGRAD) tma_prefetch(&mC);
   }
-  if (warp == 1) tmem_alloc(tmem_holder, C_::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -241,39 +275,43 @@ __global__ void __launch_bounds__(NT, 1)
     // ================================ MMA issuer ==================================
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_tf32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      const uint32_t a_lbo = A_MN ? mn.lbo : 16, b_lbo = B_MN ? mn.lbo : 16;
+      const uint32_t a_sbo = A_MN ? mn.sbo : 1024, b_sbo = B_MN ? mn.sbo : 1024;
+      const uint32_t a_lay = A_MN ? mn.layout : 2, b_lay = B_MN ? mn.layout : 2;
       int s = 0;
       uint32_t ph = 0;
-      int j = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
-        const int accb = j & 1;
-        mbar_wait(&tempty[accb], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tmem_base + accb * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+      uint32_t jb = 0;  // K blocks issued so far (selects the TMEM chunk buffer)
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb, ++jb) {
+          const uint32_t buf = jb % NBUF;
+          mbar_wait(&tempty[buf], ((jb / NBUF) & 1) ^ 1);
+          tc_fence_after();
           mbar_wait(&full_op[s], ph);
           tc_fence_after();
+          const uint32_t dcol = tmem_base + buf * BN;
           const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
           const uint32_t aH = st, aL = st + C_::A_BYTES;
           const uint32_t bH = st + 2 * C_::A_BYTES, bL = bH + C_::B_BYTES;
+          // small products first (their truncation is relative to a small partial sum) ...
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            // K offset of this K=8 slice inside the stage
             const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
             const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-            const uint32_t a_lbo = A_MN ? mn.lbo : 16, b_lbo = B_MN ? mn.lbo : 16;
-            const uint32_t a_sbo = A_MN ? mn.sbo : 1024, b_sbo = B_MN ? mn.sbo : 1024;
-            const uint32_t a_lay = A_MN ? mn.layout : 2, b_lay = B_MN ? mn.layout : 2;
-            const uint64_t dAh = sdesc(aH + ao, a_lbo, a_sbo, a_lay), dAl = sdesc(aL + ao, a_lbo, a_sbo, a_lay);
-            const uint64_t dBh = sdesc(bH + bo, b_lbo, b_sbo, b_lay), dBl = sdesc(bL + bo, b_lbo, b_sbo, b_lay);
-            const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
-            mma_tf32(dcol, dAl, dBh, IDESC, first);
-            mma_tf32(dcol, dAh, dBl, IDESC, 1u);
-            mma_tf32(dcol, dAh, dBh, IDESC, 1u);
+            mma_tf32(dcol, sdesc(aL + ao, a_lbo, a_sbo, a_lay), sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC,
+                     kk == 0 ? 0u : 1u);
+            mma_tf32(dcol, sdesc(aH + ao, a_lbo, a_sbo, a_lay), sdesc(bL + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
+          }
+          // ... then the four big ones
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
+            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
+            mma_tf32(dcol, sdesc(aH + ao, a_lbo, a_sbo, a_lay), sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
           }
           mma_commit(&empty[s]);
+          mma_commit(&tfull[buf]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
-        mma_commit(&tfull[accb]);
       }
     }
   } else if (warp < 4) {
@@ -316,108 +354,178 @@ __global__ void __launch_bounds__(NT, 1)
     }
   } else {
     // ================================ epilogue ====================================
-    const int e = threadIdx.x - 128;      // 0..127 = TMEM lane = tile row
-    const int ew = e >> 5;                // epilogue warp -> TMEM lanes [32 ew, 32 ew + 32)
-    int j = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+    const int ew = warp - 4;               // 0..7
+    const int quad = warp & 3;             // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
+    const int half = ew >> 2;              // column half of the tile
+    uint8_t* stg = stg_base + ew * STG;
+    const uint32_t t_lane = (uint32_t)(32 * quad) << 16;
+    const bool vec_ds = a.dsrc && ((a.ld_dsrc & 3) == 0) && ((a.s_dsrc & 3) == 0) && (((uintptr_t)a.dsrc & 15) == 0);
+    const bool vec_v = a.V && ((a.ldv & 3) == 0) && (((uintptr_t)a.V & 15) == 0);
+    const bool vec_sl = a.slot_w && ((a.n_in & 3) == 0) && (((uintptr_t)a.slot_w & 15) == 0);
+    uint32_t jb = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
-      const int accb = j & 1;
-      mbar_wait(&tfull[accb], (j >> 1) & 1);
-      tc_fence_after();
-      const int m = mt * BM + e;
+      // ---- fold the K-block partials into round-to-nearest fp32 sums ----
+      float acc[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) acc[i] = 0.f;
+      for (int kb = 0; kb < nk; ++kb, ++jb) {
+        const uint32_t buf = jb % NBUF;
+        mbar_wait(&tfull[buf], (jb / NBUF) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
+#pragma unroll
+        for (int c = 0; c < NC / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16(taddr + 16 * c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[16 * c + i] += __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+      }
+      // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
+      const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
       const float b0v = (a.epi == EPI_RESID && a.b0) ? a.b0[(int64_t)b * a.s_b0] : 0.f;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(32 * ew) << 16) + accb * BN + c0, v);
-        const int n0 = nt * BN + c0;
-        if (!mrow || n0 >= a.N) continue;
-        const int nmax = min(32, a.N - n0);
-        switch (a.epi) {
-          case EPI_FWD: {
-            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
-            const float* bias = a.bias ? a.bias + (int64_t)b * a.s_bias + n0 : nullptr;
-            float* D = a.D ? a.D + (int64_t)b * a.sD + (int64_t)m * a.ldd + n0 : nullptr;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < nmax) {
-                float z = v[i] + (bias ? bias[i] : 0.f);
-                if (D) D[i] = cosf(z);
-                dst[i] = act_fwd(a.act, z);
-              }
-            }
-          } break;
-          case EPI_DACT: {
-            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
-            const float* ds = a.dsrc ? a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0 : nullptr;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < nmax) {
-                float z = v[i];
-                if (a.act == ACT_TANH) { const float tt = ds[i]; z *= (1.f - tt * tt); }
-                else if (a.act == ACT_SIN) z *= ds[i];
-                dst[i] = z;
-              }
-            }
-          } break;
-          case EPI_WGRAD: {
+      for (int g = 0; g < NC / 32; ++g) {
+        const int n0 = nt * BN + half * NC + 32 * g;
+        float* v = acc + 32 * g;  // compile-time offsets after unrolling: stays in registers
+        if (a.epi == EPI_WGRAD) {
+          if (mrow && n0 < a.N) {
             const int32_t* sw = a.slot_w + (int64_t)m * a.n_in + n0;
             float* gl = a.gl + (int64_t)b * a.k;
+            const bool full = vec_sl && n0 + 32 <= a.N;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < nmax) {
-                const int sl = sw[i];
-                if (sl >= 0) gl[sl] = v[i];
+            for (int q = 0; q < 8; ++q) {
+              int4 s4;
+              if (full) s4 = __ldg(reinterpret_cast<const int4*>(sw) + q);
+              else {
+                s4.x = (n0 + 4 * q + 0 < a.N) ? sw[4 * q + 0] : -1;
+                s4.y = (n0 + 4 * q + 1 < a.N) ? sw[4 * q + 1] : -1;
+                s4.z = (n0 + 4 * q + 2 < a.N) ? sw[4 * q + 2] : -1;
+                s4.w = (n0 + 4 * q + 3 < a.N) ? sw[4 * q + 3] : -1;
+              }
+              if (s4.x >= 0) gl[s4.x] = v[4 * q];
+              if (s4.y >= 0) gl[s4.y] = v[4 * q + 1];
+              if (s4.z >= 0) gl[s4.z] = v[4 * q + 2];
+              if (s4.w >= 0) gl[s4.w] = v[4 * q + 3];
+            }
+          }
+          continue;
+        }
+        if (n0 >= a.N) continue;  // whole 32-column group outside the matrix (warp-uniform)
+        const bool fullc = n0 + 32 <= a.N;
+        if (a.epi == EPI_FWD) {
+          const float* bias = a.bias ? a.bias + (int64_t)b * a.s_bias + n0 : nullptr;
+          float* D = (a.D && mrow) ? a.D + (int64_t)b * a.sD + (int64_t)m * a.ldd + n0 : nullptr;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const bool in = n0 + i < a.N;
+            float z = v[i] + ((bias && in) ? __ldg(bias + i) : 0.f);
+            if (D && in) D[i] = cosf(z);  // cos(z) of sin layers (rare path: direct stores)
+            v[i] = act_fwd(a.act, z);
+          }
+        } else if (a.epi == EPI_DACT) {
+          if (a.act != ACT_ID) {
+            const float* ds = a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0;
+            const bool vq = vec_ds && fullc;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (mrow) {
+                if (vq) d4 = __ldg(reinterpret_cast<const float4*>(ds) + q);
+                else {
+                  if (n0 + 4 * q + 0 < a.N) d4.x = ds[4 * q + 0];
+                  if (n0 + 4 * q + 1 < a.N) d4.y = ds[4 * q + 1];
+                  if (n0 + 4 * q + 2 < a.N) d4.z = ds[4 * q + 2];
+                  if (n0 + 4 * q + 3 < a.N) d4.w = ds[4 * q + 3];
+                }
+              }
+              if (a.act == ACT_TANH) {
+                v[4 * q + 0] *= (1.f - d4.x * d4.x);
+                v[4 * q + 1] *= (1.f - d4.y * d4.y);
+                v[4 * q + 2] *= (1.f - d4.z * d4.z);
+                v[4 * q + 3] *= (1.f - d4.w * d4.w);
+              } else {
+                v[4 * q + 0] *= d4.x;
+                v[4 * q + 1] *= d4.y;
+                v[4 * q + 2] *= d4.z;
+                v[4 * q + 3] *= d4.w;
               }
             }
-          } break;
-          case EPI_RESID: {
-            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
-            const float* V = a.V + (int64_t)m * a.ldv + n0;
+          }
+        } else if (a.epi == EPI_RESID) {
+          const float* V = a.V + (int64_t)m * a.ldv + n0;
+          const bool vq = vec_v && fullc;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (i < nmax) {
-                const float o = v[i] + b0v;
-                const float r = V[i] - o;
+          for (int q = 0; q < 8; ++q) {
+            float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (mrow) {
+              if (vq) y4 = __ldg(reinterpret_cast<const float4*>(V) + q);
+              else {
+                if (n0 + 4 * q + 0 < a.N) y4.x = V[4 * q + 0];
+                if (n0 + 4 * q + 1 < a.N) y4.y = V[4 * q + 1];
+                if (n0 + 4 * q + 2 < a.N) y4.z = V[4 * q + 2];
+                if (n0 + 4 * q + 3 < a.N) y4.w = V[4 * q + 3];
+              }
+            }
+            const float yy[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * q + e;
+              if (mrow && n0 + i < a.N) {
+                const float r = yy[e] - (v[i] + b0v);
                 const float R = (float)((double)r * a.inv_s2);
-                dst[i] = R;
+                v[i] = R;
                 psq += (double)r * (double)r;
                 pr += (double)R;
+              } else {
+                v[i] = 0.f;
               }
             }
-          } break;
-          default: {
-            float* dst = a.C + (int64_t)b * a.sC + (int64_t)m * a.ldc + n0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < nmax) dst[i] = v[i];
           }
         }
+        // ---- stage (128B swizzle: 16B chunk c of row r at chunk c ^ (r & 7)) and TMA-store ----
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store3(&mC, stg, n0, mt * BM + 32 * quad, b);
+          bulk_commit();
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[accb]);
       if (a.epi == EPI_RESID) {
-        // deterministic 128-thread reduction: warp shuffles, then fixed-order sum of 4 warps
+        // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           psq += __shfl_down_sync(0xffffffffu, psq, o);
           pr += __shfl_down_sync(0xffffffffu, pr, o);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (lane == 0) { red[ew] = psq; red[4 + ew] = pr; }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (e == 0) {
-          a.part_sq[(int64_t)b * a.n_part + rem] = ((red[0] + red[1]) + red[2]) + red[3];
-          a.part_r[(int64_t)b * a.n_part + rem] = ((red[4] + red[5]) + red[6]) + red[7];
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (lane == 0) { red[ew] = psq; red[NEPI + ew] = pr; }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+          double sq = 0.0, sr = 0.0;
+          for (int w = 0; w < NEPI; ++w) { sq += red[w]; sr += red[NEPI + w]; }
+          a.part_sq[(int64_t)b * a.n_part + rem] = sq;
+          a.part_r[(int64_t)b * a.n_part + rem] = sr;
         }
       }
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, C_::TMEM_COLS);
+  if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------------- host side ---
@@ -486,6 +594,9 @@ struct TcPlanner {
       if ((a.ldb % 4) || (a.sB % 4) || !al16(a.B) || (a.sB == 0 && a.batch > 1)) return false;
     }
     if (bmn && (a.N % 32)) return false;
+    if (a.epi != EPI_WGRAD) {  // TMA store of the output
+      if (!a.C || (a.ldc % 4) || (a.sC % 4) || !al16(a.C)) return false;
+    }
     return true;
   }
 
@@ -519,6 +630,17 @@ struct TcPlanner {
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, mn_swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
+  // row-major output C(m, n) = C[m*ldc + n] per batch: dims (N, M, batch), box (32, 32, 1), 128B swizzle
+  bool map_store(CUtensorMap* m, float* base, int64_t M, int64_t N, int64_t ldc, int64_t bstride, int batch) const {
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)ldc * 4, (cuuint64_t)(bstride ? bstride : M * ldc) * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
 
@@ -558,12 +680,15 @@ struct TcPlanner {
                       : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, bn));
       mB2 = mB;
     }
+    CUtensorMap mC;
+    memset(&mC, 0, sizeof(mC));
+    if (a.epi != EPI_WGRAD) ok = ok && map_store(&mC, a.C, a.M, a.N, a.ldc, a.sC, a.batch);
     if (!ok) return false;
     const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + bn - 1) / bn) * a.batch;
     const int grid = tiles < num_sms ? tiles : num_sms;
     const bool p = pre != nullptr;
 #define TL(BN, AMN, BMN, PRE) \
-  tc::tc_gemm_kernel<BN, AMN, BMN, PRE><<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, a, mn)
+  tc::tc_gemm_kernel<BN, AMN, BMN, PRE><<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, a, mn)
 #define TLB(BN)                                      \
   if (!amn && !bmn && !p) TL(BN, false, false, false); \
   else if (!amn && !bmn && p) TL(BN, false, false, true); \
