@@ -229,6 +229,10 @@ def run_ours(args):
             d = per_class.setdefault(name, [0.0, 0.0, 0.0, 0])
             d[0] += ms; d[1] += fl; d[2] += by; d[3] += 1
     step0_total = sum(v[0] for v in per_class.values())
+    if args.breakdown and rank == 0:
+        for name, (ms, fl, by, nl) in sorted(per_class.items(), key=lambda kv: -kv[1][0]):
+            tf = fl / (ms / 1000.0) / 1e12 if ms > 0 else 0.0
+            print(f"[breakdown] {name:12s} {ms:8.3f} ms  {nl:3d} launches  {tf:7.1f} TFLOP/s", file=sys.stderr)
     dom = max(per_class.items(), key=lambda kv: kv[1][0]) if per_class else None
     peaks, peak_src = load_peaks()
     engine = abi.hmc_engine_info(ctx.ctx)
@@ -330,6 +334,7 @@ def main():
     ap.add_argument("--ref-L", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", help="per-kernel-class times of step 0 to stderr")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()

@@ -195,7 +195,7 @@ __device__ __forceinline__ void load_row32(const float* __restrict__ p, int n0, 
 // A_MN: A stored M-major (A(m,k) = A[k*lda + m]);  B_MN: B stored N-major (B(k,n) = B[k*ldb + n]);
 // B_PRE: B arrives as pre-split hi/lo planes (tensor maps mB / mB2).  mC: 3-D store map of the
 // output (box 32 x 32 x 1, 128B swizzle) for every epilogue except EPI_WGRAD.
-template <int BN, bool A_MN, bool B_MN, bool B_PRE>
+template <int BN, bool A_MN, bool B_MN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                    const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC, GemmArgs a,
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(NT, 1)
     tma_prefetch(&mA);
     tma_prefetch(&mB);
     if (B_PRE) tma_prefetch(&mB2);
-    if (a.epi != EPI_WGRAD) tma_prefetch(&mC);
+    if (EPI != EPI_WGRAD) tma_prefetch(&mC);
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
@@ -375,13 +375,17 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(&tfull[buf], (jb / NBUF) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
+        constexpr int FW = NC < 64 ? NC : 64;  // columns per TMEM round trip
 #pragma unroll
-        for (int c = 0; c < NC / 16; ++c) {
-          uint32_t r[16];
-          tmem_ld16(taddr + 16 * c, r);
+        for (int c0 = 0; c0 < NC; c0 += FW) {
+          uint32_t r[FW / 16][16];
+#pragma unroll
+          for (int c = 0; c < FW / 16; ++c) tmem_ld16(taddr + c0 + 16 * c, r[c]);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[16 * c + i] += __uint_as_float(r[i]);
+          for (int c = 0; c < FW / 16; ++c)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c0 + 16 * c + i] += __uint_as_float(r[c][i]);
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
@@ -390,12 +394,12 @@ __global__ void __launch_bounds__(NT, 1)
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
-      const float b0v = (a.epi == EPI_RESID && a.b0) ? a.b0[(int64_t)b * a.s_b0] : 0.f;
+      const float b0v = (EPI == EPI_RESID && a.b0) ? a.b0[(int64_t)b * a.s_b0] : 0.f;
 #pragma unroll
       for (int g = 0; g < NC / 32; ++g) {
         const int n0 = nt * BN + half * NC + 32 * g;
         float* v = acc + 32 * g;  // compile-time offsets after unrolling: stays in registers
-        if (a.epi == EPI_WGRAD) {
+        if (EPI == EPI_WGRAD) {
           if (mrow && n0 < a.N) {
             const int32_t* sw = a.slot_w + (int64_t)m * a.n_in + n0;
             float* gl = a.gl + (int64_t)b * a.k;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         if (n0 >= a.N) continue;  // whole 32-column group outside the matrix (warp-uniform)
         const bool fullc = n0 + 32 <= a.N;
-        if (a.epi == EPI_FWD) {
+        if (EPI == EPI_FWD) {
           const float* bias = a.bias ? a.bias + (int64_t)b * a.s_bias + n0 : nullptr;
           float* D = (a.D && mrow) ? a.D + (int64_t)b * a.sD + (int64_t)m * a.ldd + n0 : nullptr;
 #pragma unroll
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(NT, 1)
             if (D && in) D[i] = cosf(z);  // cos(z) of sin layers (rare path: direct stores)
             v[i] = act_fwd(a.act, z);
           }
-        } else if (a.epi == EPI_DACT) {
+        } else if (EPI == EPI_DACT) {
           if (a.act != ACT_ID) {
             const float* ds = a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0;
             const bool vq = vec_ds && fullc;
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(NT, 1)
               }
             }
           }
-        } else if (a.epi == EPI_RESID) {
+        } else if (EPI == EPI_RESID) {
           const float* V = a.V + (int64_t)m * a.ldv + n0;
           const bool vq = vec_v && fullc;
 #pragma unroll
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(NT, 1)
           bulk_commit();
         }
       }
-      if (a.epi == EPI_RESID) {
+      if (EPI == EPI_RESID) {
         // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -542,12 +546,42 @@ struct PreSplit {
   int64_t ld = 0, stride = 0;
 };
 
+// Kernel instantiations: (A MN-major, B MN-major, B pre-split, epilogue) combinations the hot
+// path uses (plus EPI_STORE for the debug GEMM on the four unsplit layouts).  Anything else runs
+// on the SIMT engine.
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs, tc::MnDesc);
+struct TcVariant {
+  bool amn, bmn, pre;
+  int epi;
+  TcKernel fn;
+};
+template <int BN>
+inline const TcVariant* tc_variants(int* n) {
+#define TV(AMN, BMN, PRE, EPI) {AMN, BMN, PRE, EPI, (TcKernel)tc::tc_gemm_kernel<BN, AMN, BMN, PRE, EPI>}
+  static const TcVariant v[] = {
+      TV(false, false, true, EPI_FWD),     // forward      Z = A W^T        (weights pre-split)
+      TV(false, true, true, EPI_DACT),     // input grad   G = (G W) o act'  (weights pre-split)
+      TV(true, true, false, EPI_WGRAD),    // weight grad  dW = G^T A, compacted into the k-vector
+      TV(false, false, false, EPI_RESID),  // DeepONet combine + residual
+      TV(false, true, false, EPI_DACT),    // DeepONet dB = R T
+      TV(true, true, false, EPI_DACT),     // DeepONet dT = R^T B
+      TV(false, false, false, EPI_STORE),  // debug GEMM
+      TV(false, true, false, EPI_STORE),
+      TV(true, true, false, EPI_STORE),
+      TV(true, false, false, EPI_STORE),
+  };
+#undef TV
+  *n = (int)(sizeof(v) / sizeof(v[0]));
+  return v;
+}
+
 struct TcPlanner {
   bool enabled = false;
   int num_sms = 148;
   tc::EncodeTiledFn encode = nullptr;
   tc::MnDesc mn;
   CUtensorMapSwizzle mn_swizzle = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  static constexpr int BN = 128;   // tile N (UMMA N); TMEM holds 512 / BN K-block partials
 
   void init() {
     enabled = false;
@@ -559,22 +593,27 @@ struct TcPlanner {
     if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return;
     if (p.major != 10 || p.minor != 0) return;  // sm_100a binary only
     num_sms = p.multiProcessorCount;
-    if (const char* v = getenv("HMC_MN_LBO")) mn.lbo = (uint32_t)atoi(v);
-    if (const char* v = getenv("HMC_MN_SBO")) mn.sbo = (uint32_t)atoi(v);
-    if (const char* v = getenv("HMC_MN_LAYOUT")) mn.layout = (uint32_t)atoi(v);
-    if (const char* v = getenv("HMC_MN_KSTEP")) mn.kstep = (uint32_t)atoi(v);
-    if (const char* v = getenv("HMC_MN_TMA")) mn_swizzle = atoi(v) == 32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                                                                        : CU_TENSOR_MAP_SWIZZLE_128B;
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
     encode = (tc::EncodeTiledFn)fn;
     static bool attr_done = false;
     if (!attr_done) {
-      set_attrs();
+      int n = 0;
+      const TcVariant* v = tc_variants<BN>(&n);
+      for (int i = 0; i < n; ++i)
+        cudaFuncSetAttribute((const void*)v[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<BN>::SMEM);
       attr_done = true;
     }
     enabled = true;
+  }
+
+  static const TcVariant* find(bool amn, bool bmn, bool pre, int epi) {
+    int n = 0;
+    const TcVariant* v = tc_variants<BN>(&n);
+    for (int i = 0; i < n; ++i)
+      if (v[i].amn == amn && v[i].bmn == bmn && v[i].pre == pre && v[i].epi == epi) return &v[i];
+    return nullptr;
   }
 
   static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -586,6 +625,7 @@ struct TcPlanner {
     if (a.M < 64 || a.N < 32 || a.K < 32) return false;
     if (a.batch > 65535) return false;
     const bool amn = !akm, bmn = !bkm;
+    if (!find(amn, bmn, pre != nullptr, a.epi)) return false;
     if ((a.lda % 4) || (a.sA % 4) || !al16(a.A) || (a.sA == 0 && a.batch > 1)) return false;
     if (amn && (a.M % 32)) return false;
     if (pre) {
@@ -600,12 +640,9 @@ struct TcPlanner {
     return true;
   }
 
-  static int bn_for(int N) { return N <= 128 ? 128 : 256; }
-
   int n_tiles(const GemmArgs& a, bool akm, bool bkm) const {
     if (!accepts(a, akm, bkm)) return -1;
-    const int bn = bn_for(a.N);
-    return ((a.M + tc::BM - 1) / tc::BM) * ((a.N + bn - 1) / bn);
+    return ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN);
   }
 
   const char* describe() const { return enabled ? "tcgen05-3xtf32+simt" : "simt"; }
@@ -632,7 +669,6 @@ struct TcPlanner {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, mn_swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
-
   // row-major output C(m, n) = C[m*ldc + n] per batch: dims (N, M, batch), box (32, 32, 1), 128B swizzle
   bool map_store(CUtensorMap* m, float* base, int64_t M, int64_t N, int64_t ldc, int64_t bstride, int batch) const {
     cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)batch};
@@ -644,62 +680,31 @@ struct TcPlanner {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
 
-  template <int BN, bool AMN, bool BMN, bool PRE>
-  static void set_attr_one() {
-    cudaFuncSetAttribute(tc::tc_gemm_kernel<BN, AMN, BMN, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         tc::Cfg<BN>::SMEM);
-  }
-  static void set_attrs() {
-#define SA(BN)                               \
-  set_attr_one<BN, false, false, false>();   \
-  set_attr_one<BN, false, false, true>();    \
-  set_attr_one<BN, false, true, false>();    \
-  set_attr_one<BN, false, true, true>();     \
-  set_attr_one<BN, true, true, false>();     \
-  set_attr_one<BN, true, false, false>();
-    SA(128)
-    SA(256)
-#undef SA
-  }
-
   // Returns false if a tensor map could not be encoded (caller falls back to SIMT).
   bool launch(const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const PreSplit* pre = nullptr) const {
-    const int bn = bn_for(a.N);
     const bool amn = !akm, bmn = !bkm;
-    CUtensorMap mA, mB, mB2;
+    const TcVariant* v = find(amn, bmn, pre != nullptr, a.epi);
+    if (!v) return false;
+    CUtensorMap mA, mB, mB2, mC;
     memset(&mB2, 0, sizeof(mB2));
+    memset(&mC, 0, sizeof(mC));
     bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM)
                   : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
     if (pre) {
-      ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, bn)
-                      : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, bn));
-      ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, bn)
-                      : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, bn));
+      ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, BN)
+                      : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, BN));
+      ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, BN)
+                      : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, BN));
     } else {
-      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, bn)
-                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, bn));
+      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, BN)
+                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, BN));
       mB2 = mB;
     }
-    CUtensorMap mC;
-    memset(&mC, 0, sizeof(mC));
     if (a.epi != EPI_WGRAD) ok = ok && map_store(&mC, a.C, a.M, a.N, a.ldc, a.sC, a.batch);
     if (!ok) return false;
-    const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + bn - 1) / bn) * a.batch;
+    const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN) * a.batch;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    const bool p = pre != nullptr;
-#define TL(BN, AMN, BMN, PRE) \
-  tc::tc_gemm_kernel<BN, AMN, BMN, PRE><<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, a, mn)
-#define TLB(BN)                                      \
-  if (!amn && !bmn && !p) TL(BN, false, false, false); \
-  else if (!amn && !bmn && p) TL(BN, false, false, true); \
-  else if (!amn && bmn && !p) TL(BN, false, true, false); \
-  else if (!amn && bmn && p) TL(BN, false, true, true); \
-  else if (amn && bmn && !p) TL(BN, true, true, false); \
-  else if (amn && !bmn && !p) TL(BN, true, false, false); \
-  else return false;
-    if (bn == 128) { TLB(128) } else { TLB(256) }
-#undef TLB
-#undef TL
+    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, a, mn);
     return true;
   }
 };
