@@ -48,6 +48,26 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(r);
 }
 
+// tanh in fp32 without branches (tensor-core epilogue): |x| < 0.6: x p(x^2), p a degree-5
+// least-squares-minimax fit of tanh(x)/x (max relative error 1.03e-7 in fp32 Horner); else
+// sign(x) (1 - 2 / (2^(2|x| log2 e) + 1)) (max relative error ~2.5e-7 with ex2/rcp.approx).
+__device__ __forceinline__ float tanh_acc(float x) {
+  const float ax = fabsf(x);
+  const float x2 = x * x;
+  float p = -0.005852516740560532f;
+  p = fmaf(p, x2, 0.020753972232341766f);
+  p = fmaf(p, x2, -0.0537688285112381f);
+  p = fmaf(p, x2, 0.13331690430641174f);
+  p = fmaf(p, x2, -0.3333328366279602f);
+  p = fmaf(p, x2, 1.0f);
+  const float small = p * x;
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(ax * 2.8853900817779268f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+  const float big = copysignf(fmaf(-2.0f, r, 1.0f), x);
+  return ax < 0.6f ? small : big;
+}
+
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == ACT_TANH) return tanhf(z);
   if (act == ACT_SIN) return sinf(z);

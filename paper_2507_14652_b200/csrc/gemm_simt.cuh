@@ -40,6 +40,9 @@ struct GemmArgs {
   const float* b0; int64_t s_b0;
   double inv_s2;
   double* part_sq; double* part_r; int n_part;
+  // EPI_DACT (tensor-core engine only): column sums of the output per 32-row block,
+  // colsum[b * s_colsum + (m / 32) * N + n] (bias gradient of the layer below, fused)
+  float* colsum; int64_t s_colsum;
 };
 
 template <int BM>

@@ -48,6 +48,8 @@ struct NetInfo {
   const float* input = nullptr;
   int max_w = 0;
   float* G[2] = {nullptr, nullptr};
+  float* colsum = nullptr;  // [C x ceil(rows/32) x max_w] fused bias-gradient partials
+  bool cs_ready = false;    // colsum holds the partials of the current G
 };
 
 struct DevBuf {
@@ -90,6 +92,7 @@ struct hmc_ctx {
   int n_part = 0;
   float* R = nullptr;
   float* colred = nullptr;
+  float* narrow_part = nullptr;  // pass-1 partials of the narrow-input weight gradients
   int colred_chunks = 0;
   double* d_eps = nullptr;
   Rec* d_rec = nullptr;
@@ -264,7 +267,8 @@ void prof_end(hmc_ctx* x, int id, cudaStream_t st, const std::string& name, doub
   r.bytes = bytes;
 }
 
-void launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag,
+// returns true if the tensor-core engine ran it
+bool launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag,
                  const PreSplit* pre = nullptr) {
   const int id = prof_begin(x, st);
   bool tc = x->tc.accepts(a, akm, bkm, pre);
@@ -278,6 +282,37 @@ void launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t
   const double bytes = 4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N + (double)a.M * a.N);
   x->flop_acc += flops;
   prof_end(x, id, st, std::string(tc ? "tc_" : "simt_") + tag, flops, bytes);
+  return tc;
+}
+
+bool is_narrow(const LayerInfo& L) { return L.n_in <= 8; }
+
+void launch_fwd_narrow(hmc_ctx* x, const LayerInfo& L, const float* in, int64_t s_in, cudaStream_t st) {
+  dim3 grid((unsigned)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS), x->C);
+  const float* W = x->Wd;
+#define FN(DIN_) k_fwd_narrow<DIN_><<<grid, 256, 0, st>>>(in, s_in, L.rows, L.n_out, W, x->P, L.w_off, L.bias ? L.b_off : -1, \
+                                                    L.act, L.A, L.act == ACT_SIN ? L.D : nullptr)
+  switch (L.n_in) {
+    case 1: FN(1); break; case 2: FN(2); break; case 3: FN(3); break; case 4: FN(4); break;
+    case 5: FN(5); break; case 6: FN(6); break; case 7: FN(7); break; default: FN(8); break;
+  }
+#undef FN
+  x->launches++;
+}
+
+void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const float* in, int64_t s_in,
+                         cudaStream_t st) {
+  const int nch = (int)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS);
+  dim3 grid(nch, x->C);
+#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->narrow_part, nch)
+  switch (L.n_in) {
+    case 1: WN(1); break; case 2: WN(2); break; case 3: WN(3); break; case 4: WN(4); break;
+    case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;
+  }
+#undef WN
+  k_wgrad_narrow_p2<<<x->C, 256, 0, st>>>(x->narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
+                                          L.bias ? x->d_slot + L.b_off : nullptr, x->gl, x->k);
+  x->launches += 2;
 }
 
 inline const float* layer_input(hmc_ctx* x, const NetInfo& N, int i, int64_t* stride) {
@@ -294,6 +329,14 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
   LayerInfo& L = x->layers[N.layers[i]];
   int64_t s_in;
   const float* in = layer_input(x, N, i, &s_in);
+  if (is_narrow(L)) {
+    const int id = prof_begin(x, st);
+    launch_fwd_narrow(x, L, in, s_in, st);
+    const double fl = 2.0 * x->C * L.rows * L.n_out * (double)L.n_in;
+    x->flop_acc += fl;
+    prof_end(x, id, st, "narrow_fwd", fl, 4.0 * x->C * L.rows * L.n_out);
+    return;
+  }
   GemmArgs a = gemm_base((int)L.rows, L.n_out, L.n_in, x->C);
   a.A = in; a.lda = L.n_in; a.sA = s_in;
   a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
@@ -313,7 +356,13 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
     const float* G = N.G[cur];
     int64_t s_in;
     const float* in = layer_input(x, N, i, &s_in);
-    if (L.any_active) {
+    if (L.any_active && is_narrow(L)) {
+      const int id = prof_begin(x, st);
+      launch_wgrad_narrow(x, L, G, in, s_in, st);
+      const double fl = 2.0 * x->C * L.rows * L.n_out * (double)(L.n_in + 1);
+      x->flop_acc += fl;
+      prof_end(x, id, st, "narrow_wgrad", fl, 4.0 * x->C * L.rows * L.n_out);
+    } else if (L.any_active) {
       GemmArgs a = gemm_base(L.n_out, L.n_in, (int)L.rows, x->C);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
       a.B = in; a.ldb = L.n_in; a.sB = s_in;
@@ -328,14 +377,21 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
         prof_end(x, id, st, "tc_wgrad", 2.0 * a.M * a.N * (double)a.K * a.batch,
                  4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
-        if (L.bias_active) {  // bias gradient = column sums of G (fixed-order two-pass)
+        if (L.bias_active) {  // bias gradient = column sums of G (fixed order)
           const int id2 = prof_begin(x, st);
-          const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
-          k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
-                                                           x->colred, chunks);
-          k_colred_p2<<<x->C, 256, 0, st>>>(x->colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
-                                            x->k);
-          x->launches += 2;
+          if (N.cs_ready) {  // partials from the producing GEMM's epilogue
+            const int nblk = (int)((L.rows + 31) / 32);
+            k_colsum_reduce<<<x->C, 256, 0, st>>>(N.colsum, (int64_t)nblk * L.n_out, nblk, L.n_out,
+                                                  x->d_slot + L.b_off, x->gl, x->k);
+            x->launches += 1;
+          } else {
+            const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
+            k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
+                                                             x->colred, chunks);
+            k_colred_p2<<<x->C, 256, 0, st>>>(x->colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
+                                              x->k);
+            x->launches += 2;
+          }
           prof_end(x, id2, st, "bias_grad", 1.0 * x->C * L.rows * L.n_out, 4.0 * x->C * L.rows * L.n_out);
         }
       } else {
@@ -356,7 +412,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
       PreSplit pre;
       if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo + L.q_off; pre.ld = L.n_in; pre.stride = x->Ptc; }
-      launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr);
+      if (Pv.bias_active && N.colsum) { a.colsum = N.colsum; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
+      N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
       cur ^= 1;
     }
   }
@@ -394,6 +451,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
       const LayerInfo& Pv = x->layers[N.layers[nl - 2]];
       const int64_t total = (int64_t)C * Pv.rows * Pv.n_out;
       const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+      N.cs_ready = false;
       k_rank1_dact<<<blocks, 256, 0, st>>>(x->R, x->Wd, x->P, O.w_off, Pv.A, Pv.D, Pv.act, Pv.rows, Pv.n_out,
                                            C, N.G[0]);
       x->launches++;
@@ -428,7 +486,8 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
     a.C = Nb.G[0]; a.ldc = p; a.sC = x->n_c * p;
     a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = (Bl.act == ACT_SIN) ? Bl.D : Bl.A; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
-    launch_gemm(x, a, true, false, st, "dB");
+    if (Bl.bias_active && Nb.colsum) { a.colsum = Nb.colsum; a.s_colsum = (int64_t)((x->n_c + 31) / 32) * p; }
+    Nb.cs_ready = launch_gemm(x, a, true, false, st, "dB") && a.colsum;
   }
   if (Nt.l_min >= 0) {  // dT = R^T B, times act' of the trunk output layer
     GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
@@ -436,7 +495,8 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.B = Bl.A; a.ldb = p; a.sB = x->n_c * p;
     a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
     a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
-    launch_gemm(x, a, false, false, st, "dT");
+    if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
+    Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
   }
   if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
   if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
@@ -791,6 +851,16 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     }
     x->colred = dalloc<float>(x, (size_t)C * cap, err);
   }
+  {  // narrow-input weight-gradient partials: max over narrow layers of chunks x n_out x (n_in + 1)
+    size_t cap = 0;
+    for (int ni = 0; ni < x->n_nets; ++ni)
+      for (int li : x->nets[ni].layers) {
+        const LayerInfo& L = x->layers[li];
+        if (is_narrow(L))
+          cap = std::max(cap, (size_t)((x->nets[ni].rows + NARROW_ROWS - 1) / NARROW_ROWS) * L.n_out * (L.n_in + 1));
+      }
+    x->narrow_part = dalloc<float>(x, (size_t)C * cap, err);
+  }
   x->part_sq = dalloc<double>(x, (size_t)C * x->n_part, err);
   x->part_r = dalloc<double>(x, (size_t)C * x->n_part, err);
   for (int ni = 0; ni < x->n_nets; ++ni) {
@@ -806,6 +876,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     if (N.l_min >= 0) {
       N.G[0] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       N.G[1] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
+      if (x->tc.enabled) N.colsum = dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err);
     }
   }
   CK(cudaMallocHost((void**)&x->h_rec, sizeof(Rec)));

@@ -165,6 +165,104 @@ __global__ void k_colred_p2(const float* __restrict__ part, int n_chunks, int n_
   }
 }
 
+// ---- narrow-input layers (n_in <= NARROW_MAX, the networks' first layers: 1-8 inputs) ----
+// These are HBM-bound (K = n_in is tiny), so they are plain coalesced kernels, not GEMMs.
+constexpr int NARROW_MAX = 16;
+constexpr int NARROW_ROWS = 64;  // rows per CTA
+
+// forward Z = X W^T + b, A = act(Z): thread n owns output column n (weights in
+// registers), the CTA's NARROW_ROWS input rows are staged in shared memory, stores coalesced.
+template <int DIN>
+__global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X, int64_t sX, int64_t rows, int n_out,
+                                                    const float* __restrict__ Wd, int64_t P, int64_t w_off,
+                                                    int64_t b_off, int act, float* __restrict__ A,
+                                                    float* __restrict__ D) {
+  __shared__ float xs[NARROW_ROWS * DIN];
+  const int c = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * NARROW_ROWS;
+  const int nr = (int)min((int64_t)NARROW_ROWS, rows - r0);
+  const float* Xc = X + (int64_t)c * sX + r0 * DIN;
+  for (int t = threadIdx.x; t < nr * DIN; t += blockDim.x) xs[t] = Xc[t];
+  __syncthreads();
+  const float* W = Wd + (int64_t)c * P + w_off;
+  for (int n = threadIdx.x; n < n_out; n += blockDim.x) {
+    float w[DIN];
+#pragma unroll
+    for (int i = 0; i < DIN; ++i) w[i] = W[(int64_t)n * DIN + i];
+    const float bias = (b_off >= 0) ? Wd[(int64_t)c * P + b_off + n] : 0.f;
+    float* out = A + ((int64_t)c * rows + r0) * n_out + n;
+    float* dout = D ? D + ((int64_t)c * rows + r0) * n_out + n : nullptr;
+    for (int r = 0; r < nr; ++r) {
+      float z = bias;
+#pragma unroll
+      for (int i = 0; i < DIN; ++i) z = fmaf(xs[r * DIN + i], w[i], z);
+      if (dout) dout[(int64_t)r * n_out] = cosf(z);
+      out[(int64_t)r * n_out] = (act == ACT_TANH) ? tanh_acc(z) : act_fwd(act, z);
+    }
+  }
+}
+
+// weight + bias gradient, pass 1: per chunk of NARROW_ROWS rows,
+//   part[c][chunk][o][i] = sum_r G[r][o] X[r][i] (i < DIN), part[c][chunk][o][DIN] = sum_r G[r][o]
+template <int DIN>
+__global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict__ G, int64_t sG, const float* __restrict__ X,
+                                                         int64_t sX, int64_t rows, int n_out, float* __restrict__ part,
+                                                         int n_chunks) {
+  __shared__ float xs[NARROW_ROWS * DIN];
+  const int c = blockIdx.y, ch = blockIdx.x;
+  const int64_t r0 = (int64_t)ch * NARROW_ROWS;
+  const int nr = (int)min((int64_t)NARROW_ROWS, rows - r0);
+  const float* Xc = X + (int64_t)c * sX + r0 * DIN;
+  for (int t = threadIdx.x; t < nr * DIN; t += blockDim.x) xs[t] = Xc[t];
+  __syncthreads();
+  for (int o = threadIdx.x; o < n_out; o += blockDim.x) {
+    float acc[DIN + 1];
+#pragma unroll
+    for (int i = 0; i <= DIN; ++i) acc[i] = 0.f;
+    const float* g = G + (int64_t)c * sG + r0 * n_out + o;
+    for (int r = 0; r < nr; ++r) {
+      const float gv = g[(int64_t)r * n_out];
+#pragma unroll
+      for (int i = 0; i < DIN; ++i) acc[i] = fmaf(gv, xs[r * DIN + i], acc[i]);
+      acc[DIN] += gv;
+    }
+    float* pp = part + (((int64_t)c * n_chunks + ch) * n_out + o) * (DIN + 1);
+#pragma unroll
+    for (int i = 0; i <= DIN; ++i) pp[i] = acc[i];
+  }
+}
+
+// pass 2: fixed-order sum over chunks, compaction into the k-vector (W[o][i] at o*DIN + i)
+__global__ void k_wgrad_narrow_p2(const float* __restrict__ part, int n_chunks, int n_out, int din,
+                                  const int32_t* __restrict__ slot_w, const int32_t* __restrict__ slot_b,
+                                  float* __restrict__ gl, int64_t k) {
+  const int c = blockIdx.x;
+  const int per = n_out * (din + 1);
+  for (int t = threadIdx.x; t < per; t += blockDim.x) {
+    const int o = t / (din + 1), i = t - o * (din + 1);
+    const int sl = (i < din) ? slot_w[o * din + i] : (slot_b ? slot_b[o] : -1);
+    if (sl < 0) continue;
+    float acc = 0.f;
+    for (int ch = 0; ch < n_chunks; ++ch) acc += part[((int64_t)c * n_chunks + ch) * per + t];
+    gl[(int64_t)c * k + sl] = acc;
+  }
+}
+
+// ---- bias gradient from the column partials the tensor-core input-gradient epilogue wrote
+//      (one per 32-row block): gl[c][slot_b[o]] = sum_blk colsum[c][blk][o], fixed order ----
+__global__ void k_colsum_reduce(const float* __restrict__ colsum, int64_t s_colsum, int nblk, int N,
+                                const int32_t* __restrict__ slot_b, float* __restrict__ gl, int64_t k) {
+  const int c = blockIdx.x;
+  for (int o = threadIdx.x; o < N; o += blockDim.x) {
+    const int sl = slot_b[o];
+    if (sl < 0) continue;
+    const float* p = colsum + (int64_t)c * s_colsum + o;
+    float acc = 0.f;
+    for (int blk = 0; blk < nblk; ++blk) acc += p[(int64_t)blk * N];
+    gl[(int64_t)c * k + sl] = acc;
+  }
+}
+
 // ---- per-chain fixed-order reduction of the likelihood partials: lik[c] = sum r^2; the
 //      DeepONet output-bias gradient sum_n R_n goes to its k-slot ----
 __global__ void __launch_bounds__(KT) k_reduce_partials(const double* __restrict__ part_sq,

@@ -367,9 +367,14 @@ __global__ void __launch_bounds__(NT, 1)
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
       // ---- fold the K-block partials into round-to-nearest fp32 sums ----
+      // (EPI_FWD: the sums start from the bias, loaded while the first K block is in flight)
       float acc[NC];
+      {
+        const int nb = nt * BN + half * NC;
+        const float* bias = (EPI == EPI_FWD && a.bias) ? a.bias + (int64_t)b * a.s_bias + nb : nullptr;
 #pragma unroll
-      for (int i = 0; i < NC; ++i) acc[i] = 0.f;
+        for (int i = 0; i < NC; ++i) acc[i] = (bias && nb + i < a.N) ? __ldg(bias + i) : 0.f;
+      }
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NBUF;
         mbar_wait(&tfull[buf], (jb / NBUF) & 1);
@@ -425,16 +430,15 @@ __global__ void __launch_bounds__(NT, 1)
         if (n0 >= a.N) continue;  // whole 32-column group outside the matrix (warp-uniform)
         const bool fullc = n0 + 32 <= a.N;
         if (EPI == EPI_FWD) {
-          const float* bias = a.bias ? a.bias + (int64_t)b * a.s_bias + n0 : nullptr;
-          float* D = (a.D && mrow) ? a.D + (int64_t)b * a.sD + (int64_t)m * a.ldd + n0 : nullptr;
+          if (a.act == ACT_TANH) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const bool in = n0 + i < a.N;
-            float z = v[i] + ((bias && in) ? __ldg(bias + i) : 0.f);
-            if (D && in) D[i] = cosf(z);  // cos(z) of sin layers (rare path: direct stores)
-            v[i] = act_fwd(a.act, z);
-          }
+            for (int i = 0; i < 32; ++i) v[i] = tanh_acc(v[i]);
+          }  // (sin layers run on the SIMT engine: accepts() rejects them)
         } else if (EPI == EPI_DACT) {
+          if (!mrow) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
           if (a.act != ACT_ID) {
             const float* ds = a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0;
             const bool vq = vec_ds && fullc;
@@ -505,6 +509,15 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) {
           tma_store3(&mC, stg, n0, mt * BM + 32 * quad, b);
           bulk_commit();
+        }
+        if (EPI == EPI_DACT && a.colsum) {
+          // column j of the staged 32 x 32 block summed over its rows (rows >= M hold zeros);
+          // lane j reads word (r, j) at 16B chunk (j/4) ^ (r&7): 32 distinct banks per row
+          const float* sf = reinterpret_cast<const float*>(stg);
+          float cs = 0.f;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cs += sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
+          if (n0 + lane < a.N) a.colsum[(int64_t)b * a.s_colsum + (int64_t)(mt * 4 + quad) * a.N + n0 + lane] = cs;
         }
       }
       if (EPI == EPI_RESID) {
@@ -626,6 +639,7 @@ struct TcPlanner {
     if (a.batch > 65535) return false;
     const bool amn = !akm, bmn = !bkm;
     if (!find(amn, bmn, pre != nullptr, a.epi)) return false;
+    if (a.epi == EPI_FWD && a.act == ACT_SIN) return false;
     if ((a.lda % 4) || (a.sA % 4) || !al16(a.A) || (a.sA == 0 && a.batch > 1)) return false;
     if (amn && (a.M % 32)) return false;
     if (pre) {
