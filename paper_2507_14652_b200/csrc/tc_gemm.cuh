@@ -6,11 +6,15 @@
 //   tolerance, 3xTF32 meets it).
 // Accumulation: the tensor core truncates its fp32 accumulator toward zero after every MMA
 // (measured on B200, scripts/probe_tc_rounding.py: 1 + 1.5*2^-24 -> 1.0), a bias that grows
-// with the number of MMAs per accumulator (1.7e-4 relative at K = 16384).  So every 32-wide K
-// block is accumulated in its own TMEM buffer (small products first, then the big Ah.Bh
-// products: 4 truncations at most relative to the block's partial sum) and the epilogue warps
-// fold the block partials into fp32 registers with round-to-nearest adds.  The chunk buffers
-// are ping-ponged (512 / BN of them) so the MMAs of block j+1 overlap the fold of block j.
+// with the number of MMAs per accumulator (1.7e-4 relative at K = 16384).  So:
+//   * the small products Al.Bh + Ah.Bl of a tile accumulate in their own TMEM accumulator
+//     (Dsmall): their truncation is relative to a sum 2^-11 smaller than the result;
+//   * the big products Ah.Bh accumulate over only `fold` (default 2) K blocks of 32 in a
+//     chunk accumulator (Dbig, <= 8 truncations), which the epilogue warps fold into fp32
+//     registers with round-to-nearest adds; Dbig is ping-ponged so the MMAs of chunk j+1
+//     overlap the fold of chunk j, Dsmall is ping-ponged across tiles.
+// TMEM reads are ~64 B/clk/SM (B300_MICROARCH.md), so folding every K block (64 KB per 768
+// MMA clocks at BN = 128) would cap the MMA pipe at 75 %; folding every 2 halves that.
 // Structure (persistent, one CTA per SM, 384 threads):
 //   warp 0     : TMA producer  - fp32 tiles (128B-swizzled) of A and B into a STAGES-deep ring
 //   warp 1     : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8) x 12 per K block
@@ -46,7 +50,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;           // 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // 32 / 16 KB
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int NBUF = 512 / BN;                 // TMEM K-block accumulators
+  static constexpr int NBUF = 2;                        // TMEM: 2 small-product + 2 big-product accumulators
+  static_assert(4 * BN <= 512, "TMEM holds 4 accumulators of BN columns");
   static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
   static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * STG + 512 /*barriers*/;
 };
@@ -167,6 +172,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
 // kernel arguments so the encoding is verified on the device (tests/test_gpu_engine.py).
 struct MnDesc {
   uint32_t lbo = 4096, sbo = 512, layout = 1, kstep = 1024;
+  int fold = 2;  // K blocks per big-product accumulator before the epilogue folds it
 };
 
 // Instruction descriptor for kind::tf32 with fp32 accumulation.
@@ -209,10 +215,12 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* full_raw = bar;               // [S]    TMA -> converters
   uint64_t* full_op = bar + S;            // [S]    converters -> MMA
   uint64_t* empty = bar + 2 * S;          // [S]    MMA -> TMA
-  uint64_t* tfull = bar + 3 * S;          // [NBUF] MMA -> epilogue (K-block partial ready)
-  uint64_t* tempty = bar + 3 * S + NBUF;  // [NBUF] epilogue -> MMA (partial folded)
-  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 * NBUF);
-  double* red = (double*)(bar + 3 * S + 2 * NBUF + 1);  // [2 x NEPI] epilogue reductions
+  uint64_t* tfull = bar + 3 * S;          // [2] MMA -> epilogue (big-product chunk ready)
+  uint64_t* tempty = bar + 3 * S + 2;     // [2] epilogue -> MMA (chunk folded)
+  uint64_t* sfull = bar + 3 * S + 4;      // [2] MMA -> epilogue (tile's small products ready)
+  uint64_t* sempty = bar + 3 * S + 6;     // [2] epilogue -> MMA
+  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 8);
+  double* red = (double*)(bar + 3 * S + 9);  // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -226,9 +234,11 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&full_op[s], 64);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < NBUF; ++i) {
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NEPI * 32);
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], NEPI * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
@@ -280,38 +290,44 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t a_lay = A_MN ? mn.layout : 2, b_lay = B_MN ? mn.layout : 2;
       int s = 0;
       uint32_t ph = 0;
-      uint32_t jb = 0;  // K blocks issued so far (selects the TMEM chunk buffer)
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        for (int kb = 0; kb < nk; ++kb, ++jb) {
-          const uint32_t buf = jb % NBUF;
-          mbar_wait(&tempty[buf], ((jb / NBUF) & 1) ^ 1);
+      uint32_t jc = 0, jt = 0;  // chunks / tiles issued so far (select the TMEM accumulators)
+      const int F = mn.fold;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
+        // small products Al.Bh + Ah.Bl of the whole tile accumulate in Dsmall[jt & 1]: their
+        // truncation is relative to a 2^-11 smaller sum, negligible over any K
+        const uint32_t sb = jt & 1;
+        mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dsm = tmem_base + sb * BN;
+        for (int k0 = 0; k0 < nk; k0 += F, ++jc) {
+          // big products Ah.Bh of F K blocks accumulate in Dbig[jc & 1], then get folded
+          const uint32_t bb = jc & 1;
+          mbar_wait(&tempty[bb], ((jc >> 1) & 1) ^ 1);
           tc_fence_after();
-          mbar_wait(&full_op[s], ph);
-          tc_fence_after();
-          const uint32_t dcol = tmem_base + buf * BN;
-          const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
-          const uint32_t aH = st, aL = st + C_::A_BYTES;
-          const uint32_t bH = st + 2 * C_::A_BYTES, bL = bH + C_::B_BYTES;
-          // small products first (their truncation is relative to a small partial sum) ...
+          const uint32_t dbg = tmem_base + (2 + bb) * BN;
+          const int k1 = min(nk, k0 + F);
+          for (int kb = k0; kb < k1; ++kb) {
+            mbar_wait(&full_op[s], ph);
+            tc_fence_after();
+            const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
+            const uint32_t aH = st, aL = st + C_::A_BYTES;
+            const uint32_t bH = st + 2 * C_::A_BYTES, bL = bH + C_::B_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
-            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-            mma_tf32(dcol, sdesc(aL + ao, a_lbo, a_sbo, a_lay), sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC,
-                     kk == 0 ? 0u : 1u);
-            mma_tf32(dcol, sdesc(aH + ao, a_lbo, a_sbo, a_lay), sdesc(bL + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
+              const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
+              const uint64_t dAh = sdesc(aH + ao, a_lbo, a_sbo, a_lay), dAl = sdesc(aL + ao, a_lbo, a_sbo, a_lay);
+              const uint64_t dBh = sdesc(bH + bo, b_lbo, b_sbo, b_lay), dBl = sdesc(bL + bo, b_lbo, b_sbo, b_lay);
+              mma_tf32(dsm, dAl, dBh, IDESC, (kb == 0 && kk == 0) ? 0u : 1u);
+              mma_tf32(dsm, dAh, dBl, IDESC, 1u);
+              mma_tf32(dbg, dAh, dBh, IDESC, (kb == k0 && kk == 0) ? 0u : 1u);
+            }
+            mma_commit(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
           }
-          // ... then the four big ones
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
-            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-            mma_tf32(dcol, sdesc(aH + ao, a_lbo, a_sbo, a_lay), sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
-          }
-          mma_commit(&empty[s]);
-          mma_commit(&tfull[buf]);
-          if (++s == S) { s = 0; ph ^= 1; }
+          mma_commit(&tfull[bb]);
         }
+        mma_commit(&sfull[sb]);
       }
     }
   } else if (warp < 4) {
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(NT, 1)
     const bool vec_ds = a.dsrc && ((a.ld_dsrc & 3) == 0) && ((a.s_dsrc & 3) == 0) && (((uintptr_t)a.dsrc & 15) == 0);
     const bool vec_v = a.V && ((a.ldv & 3) == 0) && (((uintptr_t)a.V & 15) == 0);
     const bool vec_sl = a.slot_w && ((a.n_in & 3) == 0) && (((uintptr_t)a.slot_w & 15) == 0);
-    uint32_t jb = 0;
+    uint32_t jc = 0, jt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
@@ -375,11 +391,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] = (bias && nb + i < a.N) ? __ldg(bias + i) : 0.f;
       }
-      for (int kb = 0; kb < nk; ++kb, ++jb) {
-        const uint32_t buf = jb % NBUF;
-        mbar_wait(&tfull[buf], (jb / NBUF) & 1);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
+      auto fold = [&](uint32_t col) {
+        const uint32_t taddr = tmem_base + t_lane + col + half * NC;
         constexpr int FW = NC < 64 ? NC : 64;  // columns per TMEM round trip
 #pragma unroll
         for (int c0 = 0; c0 < NC; c0 += FW) {
@@ -392,8 +405,23 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) acc[c0 + 16 * c + i] += __uint_as_float(r[c][i]);
         }
+      };
+      for (int k0 = 0; k0 < nk; k0 += mn.fold, ++jc) {
+        const uint32_t bb = jc & 1;
+        mbar_wait(&tfull[bb], (jc >> 1) & 1);
+        tc_fence_after();
+        fold((2 + bb) * BN);
         tc_fence_before();
-        mbar_arrive(&tempty[buf]);
+        mbar_arrive(&tempty[bb]);
+      }
+      {
+        const uint32_t sb = jt & 1;
+        mbar_wait(&sfull[sb], (jt >> 1) & 1);
+        tc_fence_after();
+        fold(sb * BN);
+        tc_fence_before();
+        mbar_arrive(&sempty[sb]);
+        ++jt;
       }
       // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
       const int m = mt * BM + 32 * quad + lane;
@@ -610,6 +638,7 @@ struct TcPlanner {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
     encode = (tc::EncodeTiledFn)fn;
+    if (const char* f = getenv("HMC_TC_FOLD")) mn.fold = std::max(1, atoi(f));
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
