@@ -524,7 +524,12 @@ void enqueue_step(hmc_ctx* x, int mode, cudaStream_t st, std::string& err) {
   enqueue_reduce(x, st, err);
   prof_end(x, idr, st, "reduce", 0.0, 0.0);
   const int idf = prof_begin(x, st);
-  k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), mode);
+  if (mode == 1) {
+    const int64_t total = (int64_t)x->C * x->k;
+    k_leapfrog<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(x->kstate());
+  } else {
+    k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), mode);
+  }
   x->launches++;
   prof_end(x, idf, st, "finalize", 0.0, 0.0);
 }

@@ -315,6 +315,27 @@ __global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
   if (threadIdx.x == 0) s.wrk_logp[c] = -s.lik[c] * s.inv_2s2 - 0.5 * ss * s.inv_sp2;
 }
 
+// ---- inner leapfrog step (Q2), all chains at once: g = g_lik - theta / sigma_p^2,
+//      full kick p += eps g, drift theta += eps M^-1 p, scatter.  log pi is not needed at the
+//      inner points (only at the trajectory end, k_finalize mode 2), so no reduction here ----
+__global__ void __launch_bounds__(256) k_leapfrog(KState s) {
+  const float fe = (float)(*s.eps);
+  const int64_t total = (int64_t)s.C * s.k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / s.k, j = t - c * s.k;
+    float th = s.wrk_theta[t];
+    const float g = s.gl[t] - (float)((double)th * s.inv_sp2);
+    s.wrk_grad[t] = g;
+    const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+    const float p = fmaf(fe, g, s.p[t]);
+    s.p[t] = p;
+    th = fmaf(fe * im, p, th);
+    s.wrk_theta[t] = th;
+    put_param(s, c, j, th);
+  }
+}
+
 // ---- start of a trajectory (Algorithm 2): p = sqrt(m) z with z from Philox
 //      (key = seed, counter = (j>>2, tag 0, iter, chain_id)), K0 = 1/2 sum p^2 / m (fp64),
 //      H0 = -log pi(theta) + K0; then the opening half kick and first drift (+ scatter).

@@ -38,20 +38,22 @@
 namespace hmc {
 namespace tc {
 
-constexpr int BM = 128;   // UMMA M (cta_group::1)
-constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
-constexpr int NT = 384;   // threads
-constexpr int NEPI = 8;   // epilogue warps
-constexpr int STG = 4096; // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
+constexpr int BM = 128;    // UMMA M (cta_group::1)
+constexpr int BK = 32;     // fp32 elements per K block (one 128-byte swizzle row)
+constexpr int NCONV = 4;   // converter warps: one per TMEM lane quadrant (A rows -> TMEM)
+constexpr int NEPI = 8;    // epilogue warps
+constexpr int NT = (2 + NCONV + NEPI) * 32;  // 448 threads
+constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = (BN == 256) ? 2 : 3;
-  static constexpr int A_BYTES = BM * BK * 4;           // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;           // 32 / 16 KB
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int NBUF = 2;                        // TMEM: 2 small-product + 2 big-product accumulators
-  static_assert(4 * BN <= 512, "TMEM holds 4 accumulators of BN columns");
+  static constexpr int STAGES = 4;
+  static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
+  static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
+  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  static constexpr int NACC = 3;                        // TMEM K-block accumulators (BN columns each)
+  static constexpr int A_COL0 = NACC * BN;              // TMEM A slots: [hi 32 | lo 32] columns x 2
+  static_assert(NACC * BN + 2 * 64 <= 512, "TMEM budget");
   static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
   static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * STG + 512 /*barriers*/;
 };
@@ -118,6 +120,31 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+// D[tmem] (+)= A[tmem] . B[smem]: A is M x 8 tf32 (TMEM lane = row, one column per K element)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// 32 lanes x 32 consecutive 32-bit columns from registers (lane i of the warp -> TMEM lane base + i)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%"
+      "28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
@@ -201,26 +228,28 @@ __device__ __forceinline__ void load_row32(const float* __restrict__ p, int n0, 
 // A_MN: A stored M-major (A(m,k) = A[k*lda + m]);  B_MN: B stored N-major (B(k,n) = B[k*ldb + n]);
 // B_PRE: B arrives as pre-split hi/lo planes (tensor maps mB / mB2).  mC: 3-D store map of the
 // output (box 32 x 32 x 1, 128B swizzle) for every epilogue except EPI_WGRAD.
+// A lands raw in shared memory (K-major: 128B swizzle; M-major: no swizzle), the converter warps
+// split it row by row into hi/lo TMEM columns (the MMA reads A from TMEM, so A costs no
+// shared-memory bandwidth beyond one read); B is read by the MMA from shared memory.
 template <int BN, bool A_MN, bool B_MN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                    const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC, GemmArgs a,
                    MnDesc mn) {
   using C_ = Cfg<BN>;
-  constexpr int S = C_::STAGES, NBUF = C_::NBUF, NC = C_::NC;
+  constexpr int S = C_::STAGES, NACC = C_::NACC, NC = C_::NC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg_base = smem + S * C_::STAGE_BYTES;
   uint64_t* bar = (uint64_t*)(stg_base + NEPI * STG);
-  uint64_t* full_raw = bar;               // [S]    TMA -> converters
-  uint64_t* full_op = bar + S;            // [S]    converters -> MMA
-  uint64_t* empty = bar + 2 * S;          // [S]    MMA -> TMA
-  uint64_t* tfull = bar + 3 * S;          // [2] MMA -> epilogue (big-product chunk ready)
-  uint64_t* tempty = bar + 3 * S + 2;     // [2] epilogue -> MMA (chunk folded)
-  uint64_t* sfull = bar + 3 * S + 4;      // [2] MMA -> epilogue (tile's small products ready)
-  uint64_t* sempty = bar + 3 * S + 6;     // [2] epilogue -> MMA
-  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 8);
-  double* red = (double*)(bar + 3 * S + 9);  // [2 x NEPI] epilogue reductions
+  uint64_t* full_raw = bar;                 // [S]    TMA -> converters
+  uint64_t* full_op = bar + S;              // [S]    converters -> MMA (A in TMEM, B split)
+  uint64_t* empty = bar + 2 * S;            // [S]    MMA -> TMA
+  uint64_t* afree = bar + 3 * S;            // [2]    MMA -> converters (TMEM A slot free)
+  uint64_t* tfull = bar + 3 * S + 2;        // [NACC] MMA -> epilogue (K-block partial ready)
+  uint64_t* tempty = bar + 3 * S + 2 + NACC;  // [NACC] epilogue -> MMA (partial folded)
+  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 + 2 * NACC);
+  double* red = (double*)(bar + 3 * S + 3 + 2 * NACC);  // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -231,14 +260,13 @@ __global__ void __launch_bounds__(NT, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full_raw[s], 1);
-      mbar_init(&full_op[s], 64);
+      mbar_init(&full_op[s], NCONV * 32);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 2; ++i) mbar_init(&afree[i], 1);
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NEPI * 32);
-      mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], NEPI * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
@@ -264,12 +292,12 @@ __global__ void __launch_bounds__(NT, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C_::STAGE_BYTES;
-          uint8_t* sAh = st;
-          uint8_t* sBh = st + 2 * C_::A_BYTES;
+          uint8_t* sA = st;
+          uint8_t* sBh = st + C_::A_BYTES;
           uint8_t* sBl = sBh + C_::B_BYTES;
           mbar_expect_tx(&full_raw[s], bytes);
-          if (A_MN) tma_load4(sAh, &mA, &full_raw[s], 0, kb * BK, mt * (BM / 32), b);
-          else tma_load3(sAh, &mA, &full_raw[s], kb * BK, mt * BM, b);
+          if (A_MN) tma_load4(sA, &mA, &full_raw[s], 0, kb * BK, mt * (BM / 32), b);
+          else tma_load3(sA, &mA, &full_raw[s], kb * BK, mt * BM, b);
           if (B_MN) {
             tma_load4(sBh, &mB, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
             if (B_PRE) tma_load4(sBl, &mB2, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
@@ -283,78 +311,62 @@ __global__ void __launch_bounds__(NT, 1)
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ==================================
+    // per K block, into the block's own accumulator (folded by the epilogue): the 8 small
+    // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
+    // ones Ah.Bh
     if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_tf32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-      const uint32_t a_lbo = A_MN ? mn.lbo : 16, b_lbo = B_MN ? mn.lbo : 16;
-      const uint32_t a_sbo = A_MN ? mn.sbo : 1024, b_sbo = B_MN ? mn.sbo : 1024;
-      const uint32_t a_lay = A_MN ? mn.layout : 2, b_lay = B_MN ? mn.layout : 2;
+      constexpr uint32_t IDESC = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
+      const uint32_t b_lbo = B_MN ? mn.lbo : 16, b_sbo = B_MN ? mn.sbo : 1024, b_lay = B_MN ? mn.layout : 2;
       int s = 0;
       uint32_t ph = 0;
-      uint32_t jc = 0, jt = 0;  // chunks / tiles issued so far (select the TMEM accumulators)
-      const int F = mn.fold;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
-        // small products Al.Bh + Ah.Bl of the whole tile accumulate in Dsmall[jt & 1]: their
-        // truncation is relative to a 2^-11 smaller sum, negligible over any K
-        const uint32_t sb = jt & 1;
-        mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dsm = tmem_base + sb * BN;
-        for (int k0 = 0; k0 < nk; k0 += F, ++jc) {
-          // big products Ah.Bh of F K blocks accumulate in Dbig[jc & 1], then get folded
-          const uint32_t bb = jc & 1;
-          mbar_wait(&tempty[bb], ((jc >> 1) & 1) ^ 1);
+      uint32_t jb = 0;  // K blocks issued so far
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb, ++jb) {
+          const uint32_t buf = jb % NACC;
+          mbar_wait(&tempty[buf], ((jb / NACC) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t dbg = tmem_base + (2 + bb) * BN;
-          const int k1 = min(nk, k0 + F);
-          for (int kb = k0; kb < k1; ++kb) {
-            mbar_wait(&full_op[s], ph);
-            tc_fence_after();
-            const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
-            const uint32_t aH = st, aL = st + C_::A_BYTES;
-            const uint32_t bH = st + 2 * C_::A_BYTES, bL = bH + C_::B_BYTES;
+          mbar_wait(&full_op[s], ph);
+          tc_fence_after();
+          const uint32_t dcol = tmem_base + buf * BN;
+          const uint32_t aH = tmem_base + C_::A_COL0 + (jb & 1) * 64, aL = aH + 32;
+          const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
+          const uint32_t bH = st + C_::A_BYTES, bL = bH + C_::B_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint32_t ao = A_MN ? kk * mn.kstep : kk * 32;
-              const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-              const uint64_t dAh = sdesc(aH + ao, a_lbo, a_sbo, a_lay), dAl = sdesc(aL + ao, a_lbo, a_sbo, a_lay);
-              const uint64_t dBh = sdesc(bH + bo, b_lbo, b_sbo, b_lay), dBl = sdesc(bL + bo, b_lbo, b_sbo, b_lay);
-              mma_tf32(dsm, dAl, dBh, IDESC, (kb == 0 && kk == 0) ? 0u : 1u);
-              mma_tf32(dsm, dAh, dBl, IDESC, 1u);
-              mma_tf32(dbg, dAh, dBh, IDESC, (kb == k0 && kk == 0) ? 0u : 1u);
-            }
-            mma_commit(&empty[s]);
-            if (++s == S) { s = 0; ph ^= 1; }
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
+            mma_tf32_ts(dcol, aL + 8 * kk, sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, kk == 0 ? 0u : 1u);
+            mma_tf32_ts(dcol, aH + 8 * kk, sdesc(bL + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
           }
-          mma_commit(&tfull[bb]);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
+            mma_tf32_ts(dcol, aH + 8 * kk, sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&afree[jb & 1]);
+          mma_commit(&tfull[buf]);
+          if (++s == S) { s = 0; ph ^= 1; }
         }
-        mma_commit(&sfull[sb]);
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 2 + NCONV) {
     // ================================ converters ==================================
-    const int ct = threadIdx.x - 64;  // 0..63
+    const int quad = warp & 3;          // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
+    const int r = 32 * quad + lane;     // the A row this thread splits
+    const int ct = threadIdx.x - 64;    // 0..127 (B planes)
+    const uint32_t ta = tmem_base + ((uint32_t)(32 * quad) << 16) + C_::A_COL0;
     int s = 0;
     uint32_t ph = 0;
+    uint32_t jb = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = 0; kb < nk; ++kb, ++jb) {
         mbar_wait(&full_raw[s], ph);
         uint8_t* st = smem + s * C_::STAGE_BYTES;
-        float4* ah = (float4*)st;
-        float4* al = (float4*)(st + C_::A_BYTES);
+        if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
+          float4* bh = (float4*)(st + C_::A_BYTES);
+          float4* bl = (float4*)(st + C_::A_BYTES + C_::B_BYTES);
 #pragma unroll 4
-        for (int i = ct; i < C_::A_BYTES / 16; i += 64) {
-          const float4 x = ah[i];
-          float4 h, l;
-          h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
-          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-          ah[i] = h;
-          al[i] = l;
-        }
-        if (!B_PRE) {
-          float4* bh = (float4*)(st + 2 * C_::A_BYTES);
-          float4* bl = (float4*)(st + 2 * C_::A_BYTES + C_::B_BYTES);
-#pragma unroll 4
-          for (int i = ct; i < C_::B_BYTES / 16; i += 64) {
+          for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
             const float4 x = bh[i];
             float4 h, l;
             h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
@@ -362,15 +374,45 @@ __global__ void __launch_bounds__(NT, 1)
             bh[i] = h;
             bl[i] = l;
           }
+          fence_proxy_async();
         }
-        fence_proxy_async();
+        uint32_t hi[32], lo[32];
+        if (!A_MN) {  // row r: 8 x 16B chunks, chunk q at q ^ (r & 7) (128B swizzle)
+          const float4* row = (const float4*)(st + r * 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 x = row[q ^ (r & 7)];
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float h = tf32_rna(xv[e]);
+              hi[4 * q + e] = __float_as_uint(h);
+              lo[4 * q + e] = __float_as_uint(xv[e] - h);
+            }
+          }
+        } else {  // [m / 32][k][m % 32], no swizzle: lanes read consecutive words
+          const float* col = (const float*)st + (r >> 5) * 1024 + (r & 31);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float x = col[k * 32];
+            const float h = tf32_rna(x);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(x - h);
+          }
+        }
+        mbar_wait(&afree[jb & 1], ((jb >> 1) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st32(ta + (jb & 1) * 64, hi);
+        tmem_st32(ta + (jb & 1) * 64 + 32, lo);
+        tmem_wait_st();
+        tc_fence_before();
         mbar_arrive(&full_op[s]);
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
   } else {
     // ================================ epilogue ====================================
-    const int ew = warp - 4;               // 0..7
+    const int ew = warp - 2 - NCONV;       // 0..7
     const int quad = warp & 3;             // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
     const int half = ew >> 2;              // column half of the tile
     uint8_t* stg = stg_base + ew * STG;
@@ -378,7 +420,7 @@ __global__ void __launch_bounds__(NT, 1)
     const bool vec_ds = a.dsrc && ((a.ld_dsrc & 3) == 0) && ((a.s_dsrc & 3) == 0) && (((uintptr_t)a.dsrc & 15) == 0);
     const bool vec_v = a.V && ((a.ldv & 3) == 0) && (((uintptr_t)a.V & 15) == 0);
     const bool vec_sl = a.slot_w && ((a.n_in & 3) == 0) && (((uintptr_t)a.slot_w & 15) == 0);
-    uint32_t jc = 0, jt = 0;
+    uint32_t jb = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
@@ -391,37 +433,25 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] = (bias && nb + i < a.N) ? __ldg(bias + i) : 0.f;
       }
-      auto fold = [&](uint32_t col) {
-        const uint32_t taddr = tmem_base + t_lane + col + half * NC;
-        constexpr int FW = NC < 64 ? NC : 64;  // columns per TMEM round trip
+      for (int kb = 0; kb < nk; ++kb, ++jb) {
+        const uint32_t buf = jb % NACC;
+        mbar_wait(&tfull[buf], (jb / NACC) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
-        for (int c0 = 0; c0 < NC; c0 += FW) {
-          uint32_t r[FW / 16][16];
-#pragma unroll
-          for (int c = 0; c < FW / 16; ++c) tmem_ld16(taddr + c0 + 16 * c, r[c]);
+        for (int c0 = 0; c0 < NC; c0 += 32) {
+          uint32_t r0[16], r1[16];
+          tmem_ld16(taddr + c0, r0);
+          tmem_ld16(taddr + c0 + 16, r1);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < FW / 16; ++c)
-#pragma unroll
-            for (int i = 0; i < 16; ++i) acc[c0 + 16 * c + i] += __uint_as_float(r[c][i]);
+          for (int i = 0; i < 16; ++i) {
+            acc[c0 + i] += __uint_as_float(r0[i]);
+            acc[c0 + 16 + i] += __uint_as_float(r1[i]);
+          }
         }
-      };
-      for (int k0 = 0; k0 < nk; k0 += mn.fold, ++jc) {
-        const uint32_t bb = jc & 1;
-        mbar_wait(&tfull[bb], (jc >> 1) & 1);
-        tc_fence_after();
-        fold((2 + bb) * BN);
         tc_fence_before();
-        mbar_arrive(&tempty[bb]);
-      }
-      {
-        const uint32_t sb = jt & 1;
-        mbar_wait(&sfull[sb], (jt >> 1) & 1);
-        tc_fence_after();
-        fold(sb * BN);
-        tc_fence_before();
-        mbar_arrive(&sempty[sb]);
-        ++jt;
+        mbar_arrive(&tempty[buf]);
       }
       // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
       const int m = mt * BM + 32 * quad + lane;
@@ -702,14 +732,16 @@ struct TcPlanner {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   // MN-major operand X(k, j) = X[k*ld + j] per batch: dims (32, K, MN/32, batch), box (32, 32, box_mn/32, 1)
+  // (plain = no swizzle: the raw A tile only the converter warps read, [j/32][k][j%32])
   bool map_mnmajor(CUtensorMap* m, const float* base, int64_t K, int64_t MN, int64_t ld, int64_t bstride,
-                   int batch, int box_mn) const {
+                   int batch, int box_mn, bool plain = false) const {
     cuuint64_t dims[4] = {32, (cuuint64_t)K, (cuuint64_t)(MN / 32), (cuuint64_t)batch};
     cuuint64_t strides[3] = {(cuuint64_t)ld * 4, 128, (cuuint64_t)(bstride ? bstride : K * ld) * 4};
     cuuint32_t box[4] = {32, 32, (cuuint32_t)(box_mn / 32), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, mn_swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, plain ? CU_TENSOR_MAP_SWIZZLE_NONE : mn_swizzle,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   // row-major output C(m, n) = C[m*ldc + n] per batch: dims (N, M, batch), box (32, 32, 1), 128B swizzle
@@ -731,7 +763,7 @@ struct TcPlanner {
     CUtensorMap mA, mB, mB2, mC;
     memset(&mB2, 0, sizeof(mB2));
     memset(&mC, 0, sizeof(mC));
-    bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM)
+    bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM, true)
                   : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
     if (pre) {
       ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, BN)
