@@ -47,7 +47,7 @@ constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = 3;
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
   static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
@@ -55,7 +55,8 @@ struct Cfg {
   static constexpr int A_COL0 = NACC * BN;              // TMEM A slots: [hi 32 | lo 32] columns x 2
   static_assert(NACC * BN + 2 * 64 <= 512, "TMEM budget");
   static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
-  static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * STG + 512 /*barriers*/;
+  static constexpr int NGRP = NC / 32;                  // 32-column groups per epilogue thread
+  static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * NGRP * STG + 512 /*barriers*/;
 };
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a) ---
@@ -234,22 +235,26 @@ __device__ __forceinline__ void load_row32(const float* __restrict__ p, int n0, 
 template <int BN, bool A_MN, bool B_MN, bool B_PRE, int EPI>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
-                   const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC, GemmArgs a,
-                   MnDesc mn) {
+                   const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC,
+                   const __grid_constant__ CUtensorMap mX, GemmArgs a, MnDesc mn) {
   using C_ = Cfg<BN>;
-  constexpr int S = C_::STAGES, NACC = C_::NACC, NC = C_::NC;
+  constexpr int S = C_::STAGES, NACC = C_::NACC, NC = C_::NC, NGRP = C_::NGRP;
+  // EPI_DACT reads act'(dsrc) and EPI_RESID reads V tile by tile: TMA-loaded (mX) into the
+  // staging buffers while the tile's K blocks are still in flight
+  const bool loadx = (EPI == EPI_RESID) || (EPI == EPI_DACT && a.act != ACT_ID);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* stg_base = smem + S * C_::STAGE_BYTES;
-  uint64_t* bar = (uint64_t*)(stg_base + NEPI * STG);
+  uint64_t* bar = (uint64_t*)(stg_base + NEPI * NGRP * STG);
   uint64_t* full_raw = bar;                 // [S]    TMA -> converters
   uint64_t* full_op = bar + S;              // [S]    converters -> MMA (A in TMEM, B split)
   uint64_t* empty = bar + 2 * S;            // [S]    MMA -> TMA
   uint64_t* afree = bar + 3 * S;            // [2]    MMA -> converters (TMEM A slot free)
   uint64_t* tfull = bar + 3 * S + 2;        // [NACC] MMA -> epilogue (K-block partial ready)
   uint64_t* tempty = bar + 3 * S + 2 + NACC;  // [NACC] epilogue -> MMA (partial folded)
-  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 + 2 * NACC);
-  double* red = (double*)(bar + 3 * S + 3 + 2 * NACC);  // [2 x NEPI] epilogue reductions
+  uint64_t* xfull = bar + 3 * S + 2 + 2 * NACC;  // [NEPI] per epilogue warp: mX tiles landed
+  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 + 2 * NACC + NEPI);
+  double* red = (double*)(bar + 3 * S + 3 + 2 * NACC + NEPI);  // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -268,11 +273,13 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NEPI * 32);
     }
+    for (int i = 0; i < NEPI; ++i) mbar_init(&xfull[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
     tma_prefetch(&mB);
     if (B_PRE) tma_prefetch(&mB2);
     if (EPI != EPI_WGRAD) tma_prefetch(&mC);
+    if (loadx) tma_prefetch(&mX);
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
@@ -415,15 +422,27 @@ __global__ void __launch_bounds__(NT, 1)
     const int ew = warp - 2 - NCONV;       // 0..7
     const int quad = warp & 3;             // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
     const int half = ew >> 2;              // column half of the tile
-    uint8_t* stg = stg_base + ew * STG;
+    uint8_t* stg0 = stg_base + ew * NGRP * STG;  // NGRP staging tiles (32 rows x 32 fp32, 128B swizzle)
     const uint32_t t_lane = (uint32_t)(32 * quad) << 16;
-    const bool vec_ds = a.dsrc && ((a.ld_dsrc & 3) == 0) && ((a.s_dsrc & 3) == 0) && (((uintptr_t)a.dsrc & 15) == 0);
-    const bool vec_v = a.V && ((a.ldv & 3) == 0) && (((uintptr_t)a.V & 15) == 0);
     const bool vec_sl = a.slot_w && ((a.n_in & 3) == 0) && (((uintptr_t)a.slot_w & 15) == 0);
-    uint32_t jb = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    uint32_t jb = 0, jt = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
+      if (lane == 0) {
+        bulk_wait_read0();  // the previous tile's stores have read the staging tiles
+        if (loadx) {
+          int nx = 0;
+          for (int g = 0; g < NGRP; ++g) nx += (nt * BN + half * NC + 32 * g < a.N) ? 1 : 0;
+          mbar_expect_tx(&xfull[ew], nx * STG);
+          for (int g = 0; g < NGRP; ++g) {
+            const int n0 = nt * BN + half * NC + 32 * g;
+            if (n0 < a.N)
+              tma_load3(stg0 + g * STG, &mX, &xfull[ew], n0, mt * BM + 32 * quad, EPI == EPI_RESID ? 0 : b);
+          }
+        }
+      }
+      __syncwarp();
       // ---- fold the K-block partials into round-to-nearest fp32 sums ----
       // (EPI_FWD: the sums start from the bias, loaded while the first K block is in flight)
       float acc[NC];
@@ -454,6 +473,7 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_arrive(&tempty[buf]);
       }
       // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
+      if (loadx) mbar_wait(&xfull[ew], jt & 1);
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
@@ -486,32 +506,23 @@ __global__ void __launch_bounds__(NT, 1)
           continue;
         }
         if (n0 >= a.N) continue;  // whole 32-column group outside the matrix (warp-uniform)
-        const bool fullc = n0 + 32 <= a.N;
+        uint8_t* stg = stg0 + g * STG;
+        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);  // row `lane`, chunk q at q ^ (lane & 7)
         if (EPI == EPI_FWD) {
           if (a.act == ACT_TANH) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = tanh_acc(v[i]);
           }  // (sin layers run on the SIMT engine: accepts() rejects them)
         } else if (EPI == EPI_DACT) {
+          // rows >= M and columns >= N of the loaded tile are zero-filled by TMA
           if (!mrow) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
           if (a.act != ACT_ID) {
-            const float* ds = a.dsrc + (int64_t)b * a.s_dsrc + (int64_t)m * a.ld_dsrc + n0;
-            const bool vq = vec_ds && fullc;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (mrow) {
-                if (vq) d4 = __ldg(reinterpret_cast<const float4*>(ds) + q);
-                else {
-                  if (n0 + 4 * q + 0 < a.N) d4.x = ds[4 * q + 0];
-                  if (n0 + 4 * q + 1 < a.N) d4.y = ds[4 * q + 1];
-                  if (n0 + 4 * q + 2 < a.N) d4.z = ds[4 * q + 2];
-                  if (n0 + 4 * q + 3 < a.N) d4.w = ds[4 * q + 3];
-                }
-              }
+              const float4 d4 = srow[q ^ (lane & 7)];
               if (a.act == ACT_TANH) {
                 v[4 * q + 0] *= (1.f - d4.x * d4.x);
                 v[4 * q + 1] *= (1.f - d4.y * d4.y);
@@ -526,20 +537,9 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         } else if (EPI == EPI_RESID) {
-          const float* V = a.V + (int64_t)m * a.ldv + n0;
-          const bool vq = vec_v && fullc;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            float4 y4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (mrow) {
-              if (vq) y4 = __ldg(reinterpret_cast<const float4*>(V) + q);
-              else {
-                if (n0 + 4 * q + 0 < a.N) y4.x = V[4 * q + 0];
-                if (n0 + 4 * q + 1 < a.N) y4.y = V[4 * q + 1];
-                if (n0 + 4 * q + 2 < a.N) y4.z = V[4 * q + 2];
-                if (n0 + 4 * q + 3 < a.N) y4.w = V[4 * q + 3];
-              }
-            }
+            const float4 y4 = srow[q ^ (lane & 7)];
             const float yy[4] = {y4.x, y4.y, y4.z, y4.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -556,10 +556,8 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         }
-        // ---- stage (128B swizzle: 16B chunk c of row r at chunk c ^ (r & 7)) and TMA-store ----
-        if (lane == 0) bulk_wait_read0();
+        // ---- stage (in place over the loaded tile, if any) and TMA-store ----
         __syncwarp();
-        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
 #pragma unroll
         for (int q = 0; q < 8; ++q) srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         fence_proxy_async();
@@ -620,7 +618,7 @@ struct PreSplit {
 // Kernel instantiations: (A MN-major, B MN-major, B pre-split, epilogue) combinations the hot
 // path uses (plus EPI_STORE for the debug GEMM on the four unsplit layouts).  Anything else runs
 // on the SIMT engine.
-typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs, tc::MnDesc);
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs, tc::MnDesc);
 struct TcVariant {
   bool amn, bmn, pre;
   int epi;
@@ -710,6 +708,10 @@ struct TcPlanner {
     if (a.epi != EPI_WGRAD) {  // TMA store of the output
       if (!a.C || (a.ldc % 4) || (a.sC % 4) || !al16(a.C)) return false;
     }
+    if (a.epi == EPI_DACT && a.act != ACT_ID) {  // TMA load of act' source
+      if (!a.dsrc || (a.ld_dsrc % 4) || (a.s_dsrc % 4) || !al16(a.dsrc)) return false;
+    }
+    if (a.epi == EPI_RESID && (!a.V || (a.ldv % 4) || !al16(a.V))) return false;
     return true;
   }
 
@@ -760,9 +762,10 @@ struct TcPlanner {
     const bool amn = !akm, bmn = !bkm;
     const TcVariant* v = find(amn, bmn, pre != nullptr, a.epi);
     if (!v) return false;
-    CUtensorMap mA, mB, mB2, mC;
+    CUtensorMap mA, mB, mB2, mC, mX;
     memset(&mB2, 0, sizeof(mB2));
     memset(&mC, 0, sizeof(mC));
+    memset(&mX, 0, sizeof(mX));
     bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM, true)
                   : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
     if (pre) {
@@ -776,10 +779,13 @@ struct TcPlanner {
       mB2 = mB;
     }
     if (a.epi != EPI_WGRAD) ok = ok && map_store(&mC, a.C, a.M, a.N, a.ldc, a.sC, a.batch);
+    if (a.epi == EPI_DACT && a.act != ACT_ID)
+      ok = ok && map_store(&mX, const_cast<float*>(a.dsrc), a.M, a.N, a.ld_dsrc, a.s_dsrc, a.batch);
+    if (a.epi == EPI_RESID) ok = ok && map_store(&mX, const_cast<float*>(a.V), a.M, a.N, a.ldv, 0, 1);
     if (!ok) return false;
     const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN) * a.batch;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, a, mn);
+    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, mX, a, mn);
     return true;
   }
 };
