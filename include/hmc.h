@@ -190,6 +190,16 @@ int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M
                    int64_t sB, float* C, int64_t ldc, int64_t sC, void* stream);
 int hmc_profile_read(hmc_ctx* ctx, int32_t max_recs, hmc_prof_rec* out, int32_t* n_out);
 
+/* Development diagnostics of the tcgen05 engine: with HMC_TC_PROF=1 in the environment at
+ * hmc_setup time, every tensor-core GEMM adds, per CTA, the clock cycles each warp role spent
+ * waiting on its pipeline barriers.  out[16 x 16] (host) receives the sums per kernel variant
+ * (row = variant index of the engine's instantiation table; slot order: TMA waiting
+ * for a free stage, MMA waiting for a free accumulator, MMA waiting for converted operands,
+ * converter waiting for TMA, converter waiting for a free TMEM A slot, epilogue waiting for an
+ * accumulator, epilogue waiting for prefetched tiles, epilogue output cycles, kernel cycles);
+ * reset != 0 zeroes them.  Returns HMC_E_CUDA on a CUDA error. */
+int hmc_debug_tc_profile(uint64_t* out, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,7 +53,8 @@ class hmc_config(ctypes.Structure):
 
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
-           "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm"]
+           "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
+           "hmc_debug_tc_profile"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -215,6 +216,22 @@ def hmc_debug_gemm(engine, a_kmajor, b_kmajor, M, N, K, batch, A, lda, sA, B, ld
     _check(lib().hmc_debug_gemm(int(engine), int(a_kmajor), int(b_kmajor), M, N, K, batch,
                                 _ptr(A, keep), lda, sA, _ptr(B, keep), ldb, sB, _ptr(C, keep), ldc, sC,
                                 _stream(stream)))
+
+
+TC_PROF_SLOTS = ["tmaA_wait_slot", "mma_wait_acc", "mma_wait_operands", "conv_wait_A", "conv_wait_aslot",
+                 "epi_wait_acc", "epi_wait_prefetch", "epi_output", "kernel_cycles", "conv_wait_B", "tmaB_wait_slot",
+                 "mma_issue"]
+
+
+def hmc_debug_tc_profile(reset: bool = False):
+    """Per-role barrier wait cycles of the tcgen05 engine (HMC_TC_PROF=1), summed over CTAs."""
+    out = (ctypes.c_uint64 * 256)()
+    L = lib()
+    L.hmc_debug_tc_profile.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+    _check(L.hmc_debug_tc_profile(out, int(bool(reset))))
+    v = list(out)
+    return {vid: dict(zip(TC_PROF_SLOTS, v[16 * vid:16 * vid + len(TC_PROF_SLOTS)])) for vid in range(16)
+            if any(v[16 * vid:16 * vid + 16])}
 
 
 def hmc_profile(ctx, enable: bool):

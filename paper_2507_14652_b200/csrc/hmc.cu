@@ -1134,6 +1134,19 @@ int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M
   return HMC_OK;
 }
 
+// dev diagnostics: per-role barrier wait cycles of the tcgen05 engine (HMC_TC_PROF=1), summed
+// over CTAs since the last reset; out[16 x 16] ([kernel variant][slot], slots: tc::TcProf)
+int hmc_debug_tc_profile(uint64_t* out, int32_t reset) {
+  unsigned long long h[16 * 16];
+  if (cudaMemcpyFromSymbol(h, tc::g_tcprof, sizeof(h)) != cudaSuccess) return HMC_E_CUDA;
+  if (out) for (int i = 0; i < 16 * 16; ++i) out[i] = h[i];
+  if (reset) {
+    memset(h, 0, sizeof(h));
+    if (cudaMemcpyToSymbol(tc::g_tcprof, h, sizeof(h)) != cudaSuccess) return HMC_E_CUDA;
+  }
+  return HMC_OK;
+}
+
 int hmc_profile(hmc_ctx* ctx, int32_t enable) {
   API_BEGIN(ctx)
   if ((enable != 0) != ctx->prof_on) {

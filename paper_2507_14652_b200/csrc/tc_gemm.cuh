@@ -15,17 +15,19 @@
 //     overlap the fold of chunk j, Dsmall is ping-ponged across tiles.
 // TMEM reads are ~64 B/clk/SM (B300_MICROARCH.md), so folding every K block (64 KB per 768
 // MMA clocks at BN = 128) would cap the MMA pipe at 75 %; folding every 2 halves that.
-// Structure (persistent, one CTA per SM, 384 threads):
-//   warp 0     : TMA producer  - fp32 tiles (128B-swizzled) of A and B into a STAGES-deep ring
-//   warp 1     : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8) x 12 per K block
-//   warps 2-3  : converters    - split the landed fp32 tiles into hi (in place) / lo planes
-//   warps 4-11 : epilogue      - fold (tcgen05.ld 32x32b) into BN/2 fp32 registers per thread
-//               (warp w: TMEM lane quadrant w%4 = 32 tile rows, column half (w-4)/4), then the
+// Structure (persistent, one CTA per SM, 448 threads):
+//   warp 0     : TMA producer  - raw fp32 A tile and the B planes into a STAGES-deep ring, plus
+//               L2 prefetches `pf` K blocks ahead (hides HBM latency the ring cannot cover)
+//   warp 1     : TMEM allocator; lane 0 issues tcgen05.mma (M=128, N=BN, K=8, A from TMEM)
+//   warps 2-5  : converters    - A rows split into hi/lo and written to TMEM (tcgen05.st);
+//               raw B planes split in shared memory (hi in place, lo beside)
+//   warps 6-13 : epilogue      - fold (tcgen05.ld 32x32b) into BN/2 fp32 registers per thread
+//               (warp w: TMEM lane quadrant w%4 = 32 tile rows, one column half), then the
 //               fused epilogue (bias+act / act' / residual^2 / masked weight-gradient
-//               compaction); outputs staged through a 128B-swizzled smem tile per warp and
-//               written with TMA bulk tensor stores (coalesced, OOB-clipped).
-// Operand layouts: K-major or MN-major (TF32 supports both in SMEM descriptors); the weights
-// arrive pre-split (hi/lo planes written by the scatter kernel).
+//               compaction); outputs staged through 128B-swizzled smem tiles and written with
+//               TMA bulk tensor stores (coalesced, OOB-clipped)
+// Operand layouts: K-major or MN-major; the weights arrive pre-split (hi/lo planes written by
+// the scatter kernel).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -42,21 +44,24 @@ constexpr int BM = 128;    // UMMA M (cta_group::1)
 constexpr int BK = 32;     // fp32 elements per K block (one 128-byte swizzle row)
 constexpr int NCONV = 4;   // converter warps: one per TMEM lane quadrant (A rows -> TMEM)
 constexpr int NEPI = 8;    // epilogue warps
-constexpr int NT = (2 + NCONV + NEPI) * 32;  // 448 threads
+constexpr int NT = (3 + NCONV + NEPI) * 32;  // 480 threads (warp 14: B producer)
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = 3;
+  static constexpr int SA = 4;                          // raw A ring (released by the converters)
+  static constexpr int SB = 3;                          // B ring (released by the MMA)
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
-  static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  static constexpr int B_STAGE = 2 * B_BYTES;           // hi + lo planes
   static constexpr int NACC = 3;                        // TMEM K-block accumulators (BN columns each)
   static constexpr int A_COL0 = NACC * BN;              // TMEM A slots: [hi 32 | lo 32] columns x 2
   static_assert(NACC * BN + 2 * 64 <= 512, "TMEM budget");
   static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
   static constexpr int NGRP = NC / 32;                  // 32-column groups per epilogue thread
-  static constexpr int SMEM = 1024 /*align*/ + STAGES * STAGE_BYTES + NEPI * NGRP * STG + 512 /*barriers*/;
+  static constexpr int B_OFF = SA * A_BYTES;
+  static constexpr int STG_OFF = B_OFF + SB * B_STAGE;
+  static constexpr int SMEM = 1024 /*align*/ + STG_OFF + NEPI * NGRP * STG + 512 /*barriers*/;
 };
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a) ---
@@ -82,6 +87,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Optional per-role stall accounting (dev diagnostics, hmc_debug_tc_profile): cycles each role
+// spends waiting on each barrier, summed over CTAs.  Slots: see TcProf below.
+enum TcProf : int { P_TMA_EMPTY = 0, P_MMA_TEMPTY, P_MMA_FULLOP, P_CONV_RAW, P_CONV_AFREE, P_EPI_TFULL, P_EPI_XFULL,
+                    P_EPI_OUT, P_TOTAL, P_CONV_B, P_BTMA_EMPTY, P_MMA_ISSUE, P_NPROF };
+__device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
+__device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
+  if (!on) { mbar_wait(b, parity); return; }
+  const unsigned long long t0 = clock64();
+  mbar_wait(b, parity);
+  acc += clock64() - t0;
+}
+
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
 }
@@ -100,7 +117,30 @@ __device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* m, uint6
       "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_pf3(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"((uint64_t)m), "r"(c0),
+               "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_pf4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"((uint64_t)m),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// one lane of a converged warp returns true (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred %%px;\n"
+      "elect.sync _|%%px, %1;\n"
+      "@%%px mov.s32 %0, 1;\n"
+      "}\n"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -200,7 +240,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
 // kernel arguments so the encoding is verified on the device (tests/test_gpu_engine.py).
 struct MnDesc {
   uint32_t lbo = 4096, sbo = 512, layout = 1, kstep = 1024;
-  int fold = 2;  // K blocks per big-product accumulator before the epilogue folds it
+  int pf = 0;    // L2 prefetch distance of the TMA producer, in K blocks (0 = off)
+  int prof = 0;  // accumulate per-role wait cycles into g_tcprof[vid]
+  int vid = 0;   // kernel variant (index in tc_variants)
 };
 
 // Instruction descriptor for kind::tf32 with fp32 accumulation.
@@ -238,23 +280,27 @@ __global__ void __launch_bounds__(NT, 1)
                    const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC,
                    const __grid_constant__ CUtensorMap mX, GemmArgs a, MnDesc mn) {
   using C_ = Cfg<BN>;
-  constexpr int S = C_::STAGES, NACC = C_::NACC, NC = C_::NC, NGRP = C_::NGRP;
+  constexpr int SA = C_::SA, SB = C_::SB, NACC = C_::NACC, NC = C_::NC, NGRP = C_::NGRP;
   // EPI_DACT reads act'(dsrc) and EPI_RESID reads V tile by tile: TMA-loaded (mX) into the
   // staging buffers while the tile's K blocks are still in flight
   const bool loadx = (EPI == EPI_RESID) || (EPI == EPI_DACT && a.act != ACT_ID);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* stg_base = smem + S * C_::STAGE_BYTES;
+  uint8_t* sAr = smem;                  // raw A ring [SA][A_BYTES]
+  uint8_t* sBr = smem + C_::B_OFF;      // B ring [SB][hi | lo]
+  uint8_t* stg_base = smem + C_::STG_OFF;
   uint64_t* bar = (uint64_t*)(stg_base + NEPI * NGRP * STG);
-  uint64_t* full_raw = bar;                 // [S]    TMA -> converters
-  uint64_t* full_op = bar + S;              // [S]    converters -> MMA (A in TMEM, B split)
-  uint64_t* empty = bar + 2 * S;            // [S]    MMA -> TMA
-  uint64_t* afree = bar + 3 * S;            // [2]    MMA -> converters (TMEM A slot free)
-  uint64_t* tfull = bar + 3 * S + 2;        // [NACC] MMA -> epilogue (K-block partial ready)
-  uint64_t* tempty = bar + 3 * S + 2 + NACC;  // [NACC] epilogue -> MMA (partial folded)
-  uint64_t* xfull = bar + 3 * S + 2 + 2 * NACC;  // [NEPI] per epilogue warp: mX tiles landed
-  uint32_t* tmem_holder = (uint32_t*)(bar + 3 * S + 2 + 2 * NACC + NEPI);
-  double* red = (double*)(bar + 3 * S + 3 + 2 * NACC + NEPI);  // [2 x NEPI] epilogue reductions
+  uint64_t* a_full = bar;                         // [SA]   TMA -> converters
+  uint64_t* a_empty = a_full + SA;                // [SA]   converters (A read) -> A producer
+  uint64_t* b_full = a_empty + SA;                // [SB]   TMA -> converters
+  uint64_t* b_empty = b_full + SB;                // [SB]   MMA -> B producer
+  uint64_t* full_op = b_empty + SB;               // [SB]   converters -> MMA (A in TMEM, B ready)
+  uint64_t* afree = full_op + SB;                 // [2]    MMA -> converters (TMEM A slot free)
+  uint64_t* tfull = afree + 2;                    // [NACC] MMA -> epilogue (K-block partial ready)
+  uint64_t* tempty = tfull + NACC;                // [NACC] epilogue -> MMA (partial folded)
+  uint64_t* xfull = tempty + NACC;                // [NEPI] per epilogue warp: mX tiles landed
+  uint32_t* tmem_holder = (uint32_t*)(xfull + NEPI);
+  double* red = (double*)(xfull + NEPI + 1);      // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -263,10 +309,14 @@ __global__ void __launch_bounds__(NT, 1)
   const int nk = (a.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full_raw[s], 1);
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], NCONV * 32);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
       mbar_init(&full_op[s], NCONV * 32);
-      mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(&afree[i], 1);
     for (int i = 0; i < NACC; ++i) {
@@ -286,33 +336,49 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  unsigned long long pacc[3] = {0ull, 0ull, 0ull};
+  const unsigned long long t_k0 = mn.prof ? clock64() : 0ull;
 
   if (warp == 0) {
-    // ================================ TMA producer ================================
+    // ============================ TMA producer: A ring ============================
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const uint32_t bytes = C_::A_BYTES + (B_PRE ? 2 : 1) * C_::B_BYTES;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
-        const int mt = rem / n_nt, nt = rem - mt * n_nt;
+        const int mt = rem / n_nt;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * C_::STAGE_BYTES;
-          uint8_t* sA = st;
-          uint8_t* sBh = st + C_::A_BYTES;
+          mbar_wait_t(&a_empty[s], ph ^ 1, mn.prof, pacc[0]);
+          uint8_t* sA = sAr + s * C_::A_BYTES;
+          mbar_expect_tx(&a_full[s], C_::A_BYTES);
+          if (A_MN) tma_load4(sA, &mA, &a_full[s], 0, kb * BK, mt * (BM / 32), b);
+          else tma_load3(sA, &mA, &a_full[s], kb * BK, mt * BM, b);
+          if (++s == SA) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2 + NCONV + NEPI) {
+    // ============================ TMA producer: B ring ============================
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t bytes = (B_PRE ? 2 : 1) * C_::B_BYTES;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
+        const int nt = rem - (rem / n_nt) * n_nt;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0]);
+          uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
-          mbar_expect_tx(&full_raw[s], bytes);
-          if (A_MN) tma_load4(sA, &mA, &full_raw[s], 0, kb * BK, mt * (BM / 32), b);
-          else tma_load3(sA, &mA, &full_raw[s], kb * BK, mt * BM, b);
+          mbar_expect_tx(&b_full[s], bytes);
           if (B_MN) {
-            tma_load4(sBh, &mB, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
-            if (B_PRE) tma_load4(sBl, &mB2, &full_raw[s], 0, kb * BK, nt * (BN / 32), b);
+            tma_load4(sBh, &mB, &b_full[s], 0, kb * BK, nt * (BN / 32), b);
+            if (B_PRE) tma_load4(sBl, &mB2, &b_full[s], 0, kb * BK, nt * (BN / 32), b);
           } else {
-            tma_load3(sBh, &mB, &full_raw[s], kb * BK, nt * BN, b);
-            if (B_PRE) tma_load3(sBl, &mB2, &full_raw[s], kb * BK, nt * BN, b);
+            tma_load3(sBh, &mB, &b_full[s], kb * BK, nt * BN, b);
+            if (B_PRE) tma_load3(sBl, &mB2, &b_full[s], kb * BK, nt * BN, b);
           }
-          if (++s == S) { s = 0; ph ^= 1; }
+          if (++s == SB) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -320,39 +386,45 @@ __global__ void __launch_bounds__(NT, 1)
     // ================================ MMA issuer ==================================
     // per K block, into the block's own accumulator (folded by the epilogue): the 8 small
     // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
-    // ones Ah.Bh
-    if (lane == 0) {
+    // ones Ah.Bh.  The whole warp runs the loop (all values warp-uniform, so they live in uniform
+    // registers); one elected lane issues the MMAs and commits.
+    {
       constexpr uint32_t IDESC = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
       const uint32_t b_lbo = B_MN ? mn.lbo : 16, b_sbo = B_MN ? mn.sbo : 1024, b_lay = B_MN ? mn.layout : 2;
+      // descriptor of stage 0's B hi plane; the address field (bits 0-13, addr >> 4) is advanced
+      // by adding byte offsets >> 4 (all shared addresses < 256 KB)
+      const uint64_t dB0 = sdesc(su32(sBr), b_lbo, b_sbo, b_lay);
+      const uint32_t kstep16 = (B_MN ? mn.kstep : 32) >> 4;
       int s = 0;
       uint32_t ph = 0;
       uint32_t jb = 0;  // K blocks issued so far
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++jb) {
           const uint32_t buf = jb % NACC;
-          mbar_wait(&tempty[buf], ((jb / NACC) & 1) ^ 1);
+          mbar_wait_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
           tc_fence_after();
-          mbar_wait(&full_op[s], ph);
+          mbar_wait_t(&full_op[s], ph, mn.prof && lane == 0, pacc[1]);
           tc_fence_after();
           const uint32_t dcol = tmem_base + buf * BN;
           const uint32_t aH = tmem_base + C_::A_COL0 + (jb & 1) * 64, aL = aH + 32;
-          const uint32_t st = su32(smem + s * C_::STAGE_BYTES);
-          const uint32_t bH = st + C_::A_BYTES, bL = bH + C_::B_BYTES;
+          const uint64_t dBh = dB0 + (uint64_t)((s * C_::B_STAGE) >> 4);
+          const uint64_t dBl = dBh + (uint64_t)(C_::B_BYTES >> 4);
+          const unsigned long long t_i0 = mn.prof ? clock64() : 0ull;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-            mma_tf32_ts(dcol, aL + 8 * kk, sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, kk == 0 ? 0u : 1u);
-            mma_tf32_ts(dcol, aH + 8 * kk, sdesc(bL + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
-          }
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              mma_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, kk == 0 ? 0u : 1u);
+              mma_tf32_ts(dcol, aH + 8 * kk, dBl + kk * kstep16, IDESC, 1u);
+            }
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t bo = B_MN ? kk * mn.kstep : kk * 32;
-            mma_tf32_ts(dcol, aH + 8 * kk, sdesc(bH + bo, b_lbo, b_sbo, b_lay), IDESC, 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
+            mma_commit(&b_empty[s]);
+            mma_commit(&afree[jb & 1]);
+            mma_commit(&tfull[buf]);
           }
-          mma_commit(&empty[s]);
-          mma_commit(&afree[jb & 1]);
-          mma_commit(&tfull[buf]);
-          if (++s == S) { s = 0; ph ^= 1; }
+          __syncwarp();
+          if (mn.prof) pacc[2] += clock64() - t_i0;
+          if (++s == SB) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -362,16 +434,16 @@ __global__ void __launch_bounds__(NT, 1)
     const int r = 32 * quad + lane;     // the A row this thread splits
     const int ct = threadIdx.x - 64;    // 0..127 (B planes)
     const uint32_t ta = tmem_base + ((uint32_t)(32 * quad) << 16) + C_::A_COL0;
-    int s = 0;
-    uint32_t ph = 0;
+    int sa = 0, sb = 0;
+    uint32_t pha = 0, phb = 0;
     uint32_t jb = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++jb) {
-        mbar_wait(&full_raw[s], ph);
-        uint8_t* st = smem + s * C_::STAGE_BYTES;
+        uint8_t* stB = sBr + sb * C_::B_STAGE;
+        mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
         if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
-          float4* bh = (float4*)(st + C_::A_BYTES);
-          float4* bl = (float4*)(st + C_::A_BYTES + C_::B_BYTES);
+          float4* bh = (float4*)stB;
+          float4* bl = (float4*)(stB + C_::B_BYTES);
 #pragma unroll 4
           for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
             const float4 x = bh[i];
@@ -383,9 +455,11 @@ __global__ void __launch_bounds__(NT, 1)
           }
           fence_proxy_async();
         }
+        mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0]);
+        const uint8_t* stA = sAr + sa * C_::A_BYTES;
         uint32_t hi[32], lo[32];
         if (!A_MN) {  // row r: 8 x 16B chunks, chunk q at q ^ (r & 7) (128B swizzle)
-          const float4* row = (const float4*)(st + r * 128);
+          const float4* row = (const float4*)(stA + r * 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 x = row[q ^ (r & 7)];
@@ -398,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         } else {  // [m / 32][k][m % 32], no swizzle: lanes read consecutive words
-          const float* col = (const float*)st + (r >> 5) * 1024 + (r & 31);
+          const float* col = (const float*)stA + (r >> 5) * 1024 + (r & 31);
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             const float x = col[k * 32];
@@ -407,17 +481,21 @@ __global__ void __launch_bounds__(NT, 1)
             lo[k] = __float_as_uint(x - h);
           }
         }
-        mbar_wait(&afree[jb & 1], ((jb >> 1) & 1) ^ 1);
+        // raw A consumed: order these generic-proxy reads before the TMA (async-proxy) refill
+        fence_proxy_async();
+        mbar_arrive(&a_empty[sa]);
+        mbar_wait_t(&afree[jb & 1], ((jb >> 1) & 1) ^ 1, mn.prof, pacc[1]);
         tc_fence_after();
         tmem_st32(ta + (jb & 1) * 64, hi);
         tmem_st32(ta + (jb & 1) * 64 + 32, lo);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&full_op[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
+        mbar_arrive(&full_op[sb]);
+        if (++sa == SA) { sa = 0; pha ^= 1; }
+        if (++sb == SB) { sb = 0; phb ^= 1; }
       }
     }
-  } else {
+  } else if (warp < 2 + NCONV + NEPI) {
     // ================================ epilogue ====================================
     const int ew = warp - 2 - NCONV;       // 0..7
     const int quad = warp & 3;             // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
@@ -429,6 +507,8 @@ __global__ void __launch_bounds__(NT, 1)
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
+      fence_proxy_async();  // this warp's reads of the staging tiles precede the TMA loads below
+      __syncwarp();
       if (lane == 0) {
         bulk_wait_read0();  // the previous tile's stores have read the staging tiles
         if (loadx) {
@@ -454,7 +534,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NACC;
-        mbar_wait(&tfull[buf], (jb / NACC) & 1);
+        mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0]);
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
@@ -473,7 +553,8 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_arrive(&tempty[buf]);
       }
       // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
-      if (loadx) mbar_wait(&xfull[ew], jt & 1);
+      if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
+      const unsigned long long t_out0 = mn.prof ? clock64() : 0ull;
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
@@ -576,6 +657,7 @@ __global__ void __launch_bounds__(NT, 1)
           if (n0 + lane < a.N) a.colsum[(int64_t)b * a.s_colsum + (int64_t)(mt * 4 + quad) * a.N + n0 + lane] = cs;
         }
       }
+      if (mn.prof) pacc[2] += clock64() - t_out0;
       if (EPI == EPI_RESID) {
         // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps
 #pragma unroll
@@ -595,6 +677,23 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     if (lane == 0) bulk_wait0();
+  }
+  if (mn.prof && lane == 0) {
+    if (warp == 0) atomicAdd(&g_tcprof[mn.vid][P_TMA_EMPTY], pacc[0]);
+    if (warp == 1) {
+      atomicAdd(&g_tcprof[mn.vid][P_MMA_TEMPTY], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_MMA_FULLOP], pacc[1]);
+      atomicAdd(&g_tcprof[mn.vid][P_MMA_ISSUE], pacc[2]);
+    }
+    if (warp == 2) {
+      atomicAdd(&g_tcprof[mn.vid][P_CONV_RAW], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_CONV_AFREE], pacc[1]);
+      atomicAdd(&g_tcprof[mn.vid][P_CONV_B], pacc[2]);
+    }
+    if (warp == 2 + NCONV + NEPI) atomicAdd(&g_tcprof[mn.vid][P_BTMA_EMPTY], pacc[0]);
+    if (warp == 2 + NCONV) {
+      atomicAdd(&g_tcprof[mn.vid][P_EPI_TFULL], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_EPI_XFULL], pacc[1]);
+      atomicAdd(&g_tcprof[mn.vid][P_EPI_OUT], pacc[2]);
+    }
+    if (warp == 0) atomicAdd(&g_tcprof[mn.vid][P_TOTAL], clock64() - t_k0);
   }
   tc_fence_before();
   __syncthreads();
@@ -666,7 +765,8 @@ struct TcPlanner {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
     encode = (tc::EncodeTiledFn)fn;
-    if (const char* f = getenv("HMC_TC_FOLD")) mn.fold = std::max(1, atoi(f));
+    if (const char* f = getenv("HMC_TC_PF")) mn.pf = std::max(0, atoi(f));
+    if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
@@ -785,7 +885,10 @@ struct TcPlanner {
     if (!ok) return false;
     const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN) * a.batch;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, mX, a, mn);
+    int nv = 0;
+    tc::MnDesc md = mn;
+    md.vid = (int)(v - tc_variants<BN>(&nv));
+    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, mX, a, md);
     return true;
   }
 };
