@@ -68,6 +68,58 @@ __device__ __forceinline__ float tanh_acc(float x) {
   return ax < 0.6f ? small : big;
 }
 
+// the same function on two values with packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2; the
+// ex2 / rcp steps stay scalar), bitwise equal to tanh_acc on each lane
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ void tanh_acc2(float& x0, float& x1) {
+  const uint64_t x = pk2(x0, x1);
+  const uint64_t x2 = fmul2(x, x);
+  uint64_t p = ffma2(pk2(-0.005852516740560532f, -0.005852516740560532f), x2,
+                     pk2(0.020753972232341766f, 0.020753972232341766f));
+  p = ffma2(p, x2, pk2(-0.0537688285112381f, -0.0537688285112381f));
+  p = ffma2(p, x2, pk2(0.13331690430641174f, 0.13331690430641174f));
+  p = ffma2(p, x2, pk2(-0.3333328366279602f, -0.3333328366279602f));
+  p = ffma2(p, x2, pk2(1.0f, 1.0f));
+  float s0, s1;
+  upk2(fmul2(p, x), s0, s1);
+  const float a0 = fabsf(x0), a1 = fabsf(x1);
+  float t0, t1;
+  upk2(fmul2(pk2(a0, a1), pk2(2.8853900817779268f, 2.8853900817779268f)), t0, t1);
+  float e0, e1, r0, r1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t1));
+  float d0, d1;
+  upk2(fadd2(pk2(e0, e1), pk2(1.0f, 1.0f)), d0, d1);
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(d0));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(d1));
+  float b0, b1;
+  upk2(ffma2(pk2(-2.0f, -2.0f), pk2(r0, r1), pk2(1.0f, 1.0f)), b0, b1);
+  x0 = a0 < 0.6f ? s0 : copysignf(b0, x0);
+  x1 = a1 < 0.6f ? s1 : copysignf(b1, x1);
+}
+
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == ACT_TANH) return tanhf(z);
   if (act == ACT_SIN) return sinf(z);

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (EPI == EPI_FWD) {
           if (a.act == ACT_TANH) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = tanh_acc(v[i]);
+            for (int i = 0; i < 32; i += 2) tanh_acc2(v[i], v[i + 1]);
           }  // (sin layers run on the SIMT engine: accepts() rejects them)
         } else if (EPI == EPI_DACT) {
           // rows >= M and columns >= N of the loaded tile are zero-filled by TMA
@@ -604,11 +604,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const float4 d4 = srow[q ^ (lane & 7)];
-              if (a.act == ACT_TANH) {
-                v[4 * q + 0] *= (1.f - d4.x * d4.x);
-                v[4 * q + 1] *= (1.f - d4.y * d4.y);
-                v[4 * q + 2] *= (1.f - d4.z * d4.z);
-                v[4 * q + 3] *= (1.f - d4.w * d4.w);
+              if (a.act == ACT_TANH) {  // v *= 1 - d^2 (packed pairs)
+                const uint64_t one = pk2(1.f, 1.f);
+                const uint64_t dxy = pk2(d4.x, d4.y), dzw = pk2(d4.z, d4.w);
+                const uint64_t fxy = ffma2(fmul2(dxy, pk2(-1.f, -1.f)), dxy, one);
+                const uint64_t fzw = ffma2(fmul2(dzw, pk2(-1.f, -1.f)), dzw, one);
+                upk2(fmul2(pk2(v[4 * q + 0], v[4 * q + 1]), fxy), v[4 * q + 0], v[4 * q + 1]);
+                upk2(fmul2(pk2(v[4 * q + 2], v[4 * q + 3]), fzw), v[4 * q + 2], v[4 * q + 3]);
               } else {
                 v[4 * q + 0] *= d4.x;
                 v[4 * q + 1] *= d4.y;
@@ -618,6 +620,11 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
         } else if (EPI == EPI_RESID) {
+          // r = V - (acc + b0), R = r / sigma^2 (stored); per 32-column group the squares and
+          // the R values are summed pairwise in fp32 (error <= 5 ulp of the group sum), the
+          // group sums accumulate in fp64
+          const float is2 = (float)a.inv_s2;
+          float sq[32], rr[32];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 y4 = srow[q ^ (lane & 7)];
@@ -625,17 +632,22 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int i = 4 * q + e;
-              if (mrow && n0 + i < a.N) {
-                const float r = yy[e] - (v[i] + b0v);
-                const float R = (float)((double)r * a.inv_s2);
-                v[i] = R;
-                psq += (double)r * (double)r;
-                pr += (double)R;
-              } else {
-                v[i] = 0.f;
-              }
+              const bool in = mrow && n0 + i < a.N;
+              const float r = in ? yy[e] - (v[i] + b0v) : 0.f;
+              v[i] = r * is2;
+              sq[i] = r * r;
+              rr[i] = v[i];
             }
           }
+#pragma unroll
+          for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+              sq[i] += sq[i + w];
+              rr[i] += rr[i + w];
+            }
+          psq += (double)sq[0];
+          pr += (double)rr[0];
         }
         // ---- stage (in place over the loaded tile, if any) and TMA-store ----
         __syncwarp();
