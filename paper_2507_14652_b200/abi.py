@@ -18,7 +18,7 @@ HMC_MLP, HMC_DEEPONET = 0, 1
 ACT = {"identity": 0, "tanh": 1, "sin": 2}
 MODE = {"single": 0, "data": 1, "chain": 2}
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
+LIB_PATH = os.environ.get("HMC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
 
 
 class HmcError(RuntimeError):
@@ -54,7 +54,7 @@ class hmc_config(ctypes.Structure):
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
-           "hmc_debug_tc_profile"]
+           "hmc_debug_tc_profile", "hmc_debug_tc_timeline"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -232,6 +232,15 @@ def hmc_debug_tc_profile(reset: bool = False):
     v = list(out)
     return {vid: dict(zip(TC_PROF_SLOTS, v[16 * vid:16 * vid + len(TC_PROF_SLOTS)])) for vid in range(16)
             if any(v[16 * vid:16 * vid + 16])}
+
+
+def hmc_debug_tc_timeline():
+    """CTA-0 timeline [8 x 256] (clock64) of the last tcgen05 GEMM with HMC_TC_PROF=2."""
+    out = (ctypes.c_uint64 * (8 * 256))()
+    L = lib()
+    L.hmc_debug_tc_timeline.argtypes = [ctypes.c_void_p]
+    _check(L.hmc_debug_tc_timeline(out))
+    return np.array(list(out), dtype=np.int64).reshape(8, 256)
 
 
 def hmc_profile(ctx, enable: bool):

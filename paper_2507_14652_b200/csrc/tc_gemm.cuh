@@ -44,7 +44,10 @@ constexpr int BM = 128;    // UMMA M (cta_group::1)
 constexpr int BK = 32;     // fp32 elements per K block (one 128-byte swizzle row)
 constexpr int NCONV = 4;   // converter warps: one per TMEM lane quadrant (A rows -> TMEM)
 constexpr int NEPI = 8;    // epilogue warps
-constexpr int NT = (3 + NCONV + NEPI) * 32;  // 480 threads (warp 14: B producer)
+constexpr int NT = (3 + NCONV + NEPI) * 32;  // 480 threads
+// Warp roles.  The warp schedulers favour higher warp ids, so the latency-critical single-lane
+// roles get the highest ids: epilogue 0-7, converters 8-11, A producer 12, B producer 13, MMA 14.
+constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TMA_A + 1, W_MMA = W_TMA_B + 1;
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
 template <int BN>
@@ -54,9 +57,13 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
   static constexpr int B_STAGE = 2 * B_BYTES;           // hi + lo planes
-  static constexpr int NACC = 3;                        // TMEM K-block accumulators (BN columns each)
-  static constexpr int A_COL0 = NACC * BN;              // TMEM A slots: [hi 32 | lo 32] columns x 2
-  static_assert(NACC * BN + 2 * 64 <= 512, "TMEM budget");
+#ifndef TC_NACC
+#define TC_NACC 2
+#endif
+  static constexpr int NACC = TC_NACC;                  // TMEM K-block accumulators (BN columns each)
+  static constexpr int NAS = (512 - NACC * BN) / 64;    // TMEM A slots: [hi 32 | lo 32] columns each
+  static constexpr int A_COL0 = NACC * BN;
+  static_assert(NACC * BN + NAS * 64 <= 512, "TMEM budget");
   static constexpr int NC = BN / 2;                     // fp32 columns per epilogue thread
   static constexpr int NGRP = NC / 32;                  // 32-column groups per epilogue thread
   static constexpr int B_OFF = SA * A_BYTES;
@@ -92,6 +99,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 enum TcProf : int { P_TMA_EMPTY = 0, P_MMA_TEMPTY, P_MMA_FULLOP, P_CONV_RAW, P_CONV_AFREE, P_EPI_TFULL, P_EPI_XFULL,
                     P_EPI_OUT, P_TOTAL, P_CONV_B, P_BTMA_EMPTY, P_MMA_ISSUE, P_NPROF };
 __device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
+// timeline of CTA 0 (prof == 2): [event][k block], events: 0 MMA loop top, 1 tempty ok,
+// 2 full_op ok, 3 issued, 4 epilogue tfull ok, 5 epilogue folded, 6 converter full (A) ok,
+// 7 converter arrive full_op
+constexpr int TL_N = 256;
+__device__ unsigned long long g_tctl[8][TL_N];
 __device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
   if (!on) { mbar_wait(b, parity); return; }
   const unsigned long long t0 = clock64();
@@ -214,10 +226,11 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// rna_tf32(x) (round to nearest, ties away) by integer rounding of the 13 dropped bits; equal to
+// cvt.rna.tf32.f32 for finite x (2 instructions instead of 4); non-finite inputs stay
+// non-finite in hi or lo = x - hi, so NaN / Inf still propagate through the product
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
 
 // SMEM matrix descriptor, SWIZZLE_128B, sm_100 version bit.
@@ -284,8 +297,10 @@ __global__ void __launch_bounds__(NT, 1)
   // EPI_DACT reads act'(dsrc) and EPI_RESID reads V tile by tile: TMA-loaded (mX) into the
   // staging buffers while the tile's K blocks are still in flight
   const bool loadx = (EPI == EPI_RESID) || (EPI == EPI_DACT && a.act != ACT_ID);
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned base, derived from the shared array by an offset so that every access
+  // below compiles to LDS/STS (a pointer rebuilt from an integer would be generic)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sAr = smem;                  // raw A ring [SA][A_BYTES]
   uint8_t* sBr = smem + C_::B_OFF;      // B ring [SB][hi | lo]
   uint8_t* stg_base = smem + C_::STG_OFF;
@@ -294,9 +309,11 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* a_empty = a_full + SA;                // [SA]   converters (A read) -> A producer
   uint64_t* b_full = a_empty + SA;                // [SB]   TMA -> converters
   uint64_t* b_empty = b_full + SB;                // [SB]   MMA -> B producer
-  uint64_t* full_op = b_empty + SB;               // [SB]   converters -> MMA (A in TMEM, B ready)
-  uint64_t* afree = full_op + SB;                 // [2]    MMA -> converters (TMEM A slot free)
-  uint64_t* tfull = afree + 2;                    // [NACC] MMA -> epilogue (K-block partial ready)
+  // converters -> MMA (A in TMEM, raw B split), one per TMEM A slot: the converters run ahead
+  // by at most NAS K blocks (afree), so a slot's barrier can never be two phases ahead
+  uint64_t* full_op = b_empty + SB;               // [NAS]
+  uint64_t* afree = full_op + C_::NAS;            // [NAS]  MMA -> converters (TMEM A slot free)
+  uint64_t* tfull = afree + C_::NAS;              // [NACC] MMA -> epilogue (K-block partial ready)
   uint64_t* tempty = tfull + NACC;                // [NACC] epilogue -> MMA (partial folded)
   uint64_t* xfull = tempty + NACC;                // [NEPI] per epilogue warp: mX tiles landed
   uint32_t* tmem_holder = (uint32_t*)(xfull + NEPI);
@@ -316,9 +333,11 @@ __global__ void __launch_bounds__(NT, 1)
     for (int s = 0; s < SB; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
-      mbar_init(&full_op[s], NCONV * 32);
     }
-    for (int i = 0; i < 2; ++i) mbar_init(&afree[i], 1);
+    for (int i = 0; i < C_::NAS; ++i) {
+      mbar_init(&full_op[i], NCONV * 32);
+      mbar_init(&afree[i], 1);
+    }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NEPI * 32);
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (EPI != EPI_WGRAD) tma_prefetch(&mC);
     if (loadx) tma_prefetch(&mX);
   }
-  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -339,7 +358,7 @@ __global__ void __launch_bounds__(NT, 1)
   unsigned long long pacc[3] = {0ull, 0ull, 0ull};
   const unsigned long long t_k0 = mn.prof ? clock64() : 0ull;
 
-  if (warp == 0) {
+  if (warp == W_TMA_A) {
     // ============================ TMA producer: A ring ============================
     if (lane == 0) {
       int s = 0;
@@ -357,17 +376,19 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp == 2 + NCONV + NEPI) {
+  } else if (warp == W_TMA_B) {
     // ============================ TMA producer: B ring ============================
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       const uint32_t bytes = (B_PRE ? 2 : 1) * C_::B_BYTES;
+      uint32_t jq = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
         const int nt = rem - (rem / n_nt) * n_nt;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = 0; kb < nk; ++kb, ++jq) {
           mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0]);
+          if (mn.prof == 2 && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
           mbar_expect_tx(&b_full[s], bytes);
@@ -382,7 +403,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ================================ MMA issuer ==================================
     // per K block, into the block's own accumulator (folded by the epilogue): the 8 small
     // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
@@ -401,12 +422,17 @@ __global__ void __launch_bounds__(NT, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++jb) {
           const uint32_t buf = jb % NACC;
+          const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+
           mbar_wait_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
+          if (tl) g_tctl[1][jb] = clock64();
           tc_fence_after();
-          mbar_wait_t(&full_op[s], ph, mn.prof && lane == 0, pacc[1]);
+          mbar_wait_t(&full_op[jb % C_::NAS], (jb / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
+          if (B_PRE) mbar_wait(&b_full[s], ph);  // (raw B planes are waited for by the converters)
+          if (tl) g_tctl[2][jb] = clock64();
           tc_fence_after();
           const uint32_t dcol = tmem_base + buf * BN;
-          const uint32_t aH = tmem_base + C_::A_COL0 + (jb & 1) * 64, aL = aH + 32;
+          const uint32_t aH = tmem_base + C_::A_COL0 + (jb % C_::NAS) * 64, aL = aH + 32;
           const uint64_t dBh = dB0 + (uint64_t)((s * C_::B_STAGE) >> 4);
           const uint64_t dBl = dBh + (uint64_t)(C_::B_BYTES >> 4);
           const unsigned long long t_i0 = mn.prof ? clock64() : 0ull;
@@ -419,43 +445,31 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
             mma_commit(&b_empty[s]);
-            mma_commit(&afree[jb & 1]);
+            mma_commit(&afree[jb % C_::NAS]);
             mma_commit(&tfull[buf]);
           }
           __syncwarp();
           if (mn.prof) pacc[2] += clock64() - t_i0;
+          if (tl) g_tctl[3][jb] = clock64();
           if (++s == SB) { s = 0; ph ^= 1; }
         }
       }
     }
-  } else if (warp < 2 + NCONV) {
+  } else if (warp >= W_CONV0) {
     // ================================ converters ==================================
     const int quad = warp & 3;          // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
     const int r = 32 * quad + lane;     // the A row this thread splits
-    const int ct = threadIdx.x - 64;    // 0..127 (B planes)
+    const int ct = threadIdx.x - 32 * W_CONV0;  // 0..127 (B planes)
     const uint32_t ta = tmem_base + ((uint32_t)(32 * quad) << 16) + C_::A_COL0;
     int sa = 0, sb = 0;
     uint32_t pha = 0, phb = 0;
     uint32_t jb = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++jb) {
-        uint8_t* stB = sBr + sb * C_::B_STAGE;
-        mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
-        if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
-          float4* bh = (float4*)stB;
-          float4* bl = (float4*)(stB + C_::B_BYTES);
-#pragma unroll 4
-          for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
-            const float4 x = bh[i];
-            float4 h, l;
-            h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
-            l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-            bh[i] = h;
-            bl[i] = l;
-          }
-          fence_proxy_async();
-        }
+        // A first (the TMEM slot write is the long pole), then raw B planes if any
         mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0]);
+        const bool tlc = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+        if (tlc) atomicMax(&g_tctl[6][jb], clock64());  // last converter warp has A
         const uint8_t* stA = sAr + sa * C_::A_BYTES;
         uint32_t hi[32], lo[32];
         if (!A_MN) {  // row r: 8 x 16B chunks, chunk q at q ^ (r & 7) (128B swizzle)
@@ -481,48 +495,115 @@ __global__ void __launch_bounds__(NT, 1)
             lo[k] = __float_as_uint(x - h);
           }
         }
-        // raw A consumed: order these generic-proxy reads before the TMA (async-proxy) refill
-        fence_proxy_async();
-        mbar_arrive(&a_empty[sa]);
-        mbar_wait_t(&afree[jb & 1], ((jb >> 1) & 1) ^ 1, mn.prof, pacc[1]);
+        const uint32_t as = jb % C_::NAS;
+        mbar_wait_t(&afree[as], ((jb / C_::NAS) & 1) ^ 1, mn.prof, pacc[1]);
         tc_fence_after();
-        tmem_st32(ta + (jb & 1) * 64, hi);
-        tmem_st32(ta + (jb & 1) * 64 + 32, lo);
+        tmem_st32(ta + as * 64, hi);
+        tmem_st32(ta + as * 64 + 32, lo);
+        if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
+          uint8_t* stB = sBr + sb * C_::B_STAGE;
+          mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
+          if (mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0) atomicMax(&g_tctl[4][jb], clock64());
+          float4* bh = (float4*)stB;
+          float4* bl = (float4*)(stB + C_::B_BYTES);
+#pragma unroll 4
+          for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
+            const float4 x = bh[i];
+            float4 h, l;
+            h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+            l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+            bh[i] = h;
+            bl[i] = l;
+          }
+        }
+        // publish: A in TMEM (wait::st), B planes visible to the async proxy (the proxy fence
+        // also orders this warp's raw-A reads before the A producer's next TMA write)
         tmem_wait_st();
+        fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&full_op[sb]);
+        mbar_arrive(&full_op[as]);
+        if (tlc) atomicMax(&g_tctl[7][jb], clock64());  // last converter warp published
+        mbar_arrive(&a_empty[sa]);
         if (++sa == SA) { sa = 0; pha ^= 1; }
         if (++sb == SB) { sb = 0; phb ^= 1; }
       }
     }
-  } else if (warp < 2 + NCONV + NEPI) {
+  } else {
     // ================================ epilogue ====================================
-    const int ew = warp - 2 - NCONV;       // 0..7
+    // Per tile: fold the K-block partials, then at the tile end apply the part of the fused
+    // epilogue that needs the registers (act' product / residual / store of the sums) and park
+    // the tile in the staging buffers; the rest (tanh for EPI_FWD, bias-gradient column sums,
+    // the TMA stores) is emitted one 32-column group at a time between the folds of the NEXT
+    // tile, so the MMA never waits for a tile's output work.
+    const int ew = warp - W_EPI0;          // 0..7
     const int quad = warp & 3;             // TMEM lane quadrant = tile rows [32 quad, 32 quad + 32)
     const int half = ew >> 2;              // column half of the tile
     uint8_t* stg0 = stg_base + ew * NGRP * STG;  // NGRP staging tiles (32 rows x 32 fp32, 128B swizzle)
     const uint32_t t_lane = (uint32_t)(32 * quad) << 16;
     const bool vec_sl = a.slot_w && ((a.n_in & 3) == 0) && (((uintptr_t)a.slot_w & 15) == 0);
+    float4* srow_base = reinterpret_cast<float4*>(stg0 + lane * 128);  // row `lane`, chunk q at q ^ (lane & 7)
+    // parked tile: pend groups left (emitted in order), its batch / row block / first column
+    int pend = 0, p_next = 0, p_b = 0, p_m0 = 0, p_nb = 0, p_blk = 0, p_ng = 0;
+    auto emit_group = [&](int g) {
+      uint8_t* stg = stg0 + g * STG;
+      float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
+      const int n0 = p_nb + 32 * g;
+      if (EPI == EPI_FWD && a.act == ACT_TANH) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 z = srow[q ^ (lane & 7)];
+          tanh_acc2(z.x, z.y);
+          tanh_acc2(z.z, z.w);
+          srow[q ^ (lane & 7)] = z;
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store3(&mC, stg, n0, p_m0, p_b);
+        bulk_commit();
+      }
+      if (EPI == EPI_DACT && a.colsum) {
+        // column j of the staged 32 x 32 block summed over its rows (rows >= M hold zeros);
+        // lane j reads word (r, j) at 16B chunk (j/4) ^ (r&7): 32 distinct banks per row
+        const float* sf = reinterpret_cast<const float*>(stg);
+        float cs = 0.f;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) cs += sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
+        if (n0 + lane < a.N) a.colsum[(int64_t)p_b * a.s_colsum + (int64_t)p_blk * a.N + n0 + lane] = cs;
+      }
+    };
+    // staging free for TMA loads / new parked tiles: all groups emitted and their stores have
+    // read the staging tiles (this warp's generic reads ordered before the async-proxy writes)
+    auto staging_free = [&]() {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    };
+    auto issue_prefetch = [&](int b, int mt, int nt) {
+      if (lane == 0) {
+        int nx = 0;
+        for (int g = 0; g < NGRP; ++g) nx += (nt * BN + half * NC + 32 * g < a.N) ? 1 : 0;
+        mbar_expect_tx(&xfull[ew], nx * STG);
+        for (int g = 0; g < NGRP; ++g) {
+          const int n0 = nt * BN + half * NC + 32 * g;
+          if (n0 < a.N)
+            tma_load3(stg0 + g * STG, &mX, &xfull[ew], n0, mt * BM + 32 * quad, EPI == EPI_RESID ? 0 : b);
+        }
+      }
+      __syncwarp();
+    };
     uint32_t jb = 0, jt = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
       const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
       const int mt = rem / n_nt, nt = rem - mt * n_nt;
-      fence_proxy_async();  // this warp's reads of the staging tiles precede the TMA loads below
-      __syncwarp();
-      if (lane == 0) {
-        bulk_wait_read0();  // the previous tile's stores have read the staging tiles
-        if (loadx) {
-          int nx = 0;
-          for (int g = 0; g < NGRP; ++g) nx += (nt * BN + half * NC + 32 * g < a.N) ? 1 : 0;
-          mbar_expect_tx(&xfull[ew], nx * STG);
-          for (int g = 0; g < NGRP; ++g) {
-            const int n0 = nt * BN + half * NC + 32 * g;
-            if (n0 < a.N)
-              tma_load3(stg0 + g * STG, &mX, &xfull[ew], n0, mt * BM + 32 * quad, EPI == EPI_RESID ? 0 : b);
-          }
-        }
+      bool prefetched = false;
+      if (loadx && pend == 0) {
+        staging_free();
+        issue_prefetch(b, mt, nt);
+        prefetched = true;
       }
-      __syncwarp();
       // ---- fold the K-block partials into round-to-nearest fp32 sums ----
       // (EPI_FWD: the sums start from the bias, loaded while the first K block is in flight)
       float acc[NC];
@@ -535,6 +616,9 @@ __global__ void __launch_bounds__(NT, 1)
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NACC;
         mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0]);
+        const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
+        const bool tla = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
@@ -551,14 +635,35 @@ __global__ void __launch_bounds__(NT, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
+        if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
+        if (pend > 0) {  // one group of the parked tile per K block
+          const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
+          emit_group(p_next++);
+          if (--pend == 0 && loadx && !prefetched) {
+            staging_free();
+            issue_prefetch(b, mt, nt);
+            prefetched = true;
+          }
+          if (mn.prof) pacc[2] += clock64() - t_e0;
+        }
       }
-      // ---- fused epilogue on the tile (rows m, columns n0 .. n0 + NC) ----
-      if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
       const unsigned long long t_out0 = mn.prof ? clock64() : 0ull;
+      while (pend > 0) {  // short K: flush the parked tile
+        emit_group(p_next++);
+        --pend;
+      }
+      if (loadx && !prefetched) {
+        staging_free();
+        issue_prefetch(b, mt, nt);
+      }
+      if (!loadx) staging_free();
+      // ---- tile end: the register part of the fused epilogue, parked in staging ----
+      if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
       const float b0v = (EPI == EPI_RESID && a.b0) ? a.b0[(int64_t)b * a.s_b0] : 0.f;
+      int ng = 0;
 #pragma unroll
       for (int g = 0; g < NC / 32; ++g) {
         const int n0 = nt * BN + half * NC + 32 * g;
@@ -587,14 +692,9 @@ __global__ void __launch_bounds__(NT, 1)
           continue;
         }
         if (n0 >= a.N) continue;  // whole 32-column group outside the matrix (warp-uniform)
-        uint8_t* stg = stg0 + g * STG;
-        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);  // row `lane`, chunk q at q ^ (lane & 7)
-        if (EPI == EPI_FWD) {
-          if (a.act == ACT_TANH) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) tanh_acc2(v[i], v[i + 1]);
-          }  // (sin layers run on the SIMT engine: accepts() rejects them)
-        } else if (EPI == EPI_DACT) {
+        ++ng;
+        float4* srow = srow_base + g * (STG / 16);
+        if (EPI == EPI_DACT) {
           // rows >= M and columns >= N of the loaded tile are zero-filled by TMA
           if (!mrow) {
 #pragma unroll
@@ -649,25 +749,14 @@ __global__ void __launch_bounds__(NT, 1)
           psq += (double)sq[0];
           pr += (double)rr[0];
         }
-        // ---- stage (in place over the loaded tile, if any) and TMA-store ----
         __syncwarp();
 #pragma unroll
         for (int q = 0; q < 8; ++q) srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        fence_proxy_async();
+      }
+      if (EPI != EPI_WGRAD) {  // park the tile
+        pend = ng; p_next = 0; p_b = b; p_m0 = mt * BM + 32 * quad; p_nb = nt * BN + half * NC;
+        p_blk = mt * 4 + quad;
         __syncwarp();
-        if (lane == 0) {
-          tma_store3(&mC, stg, n0, mt * BM + 32 * quad, b);
-          bulk_commit();
-        }
-        if (EPI == EPI_DACT && a.colsum) {
-          // column j of the staged 32 x 32 block summed over its rows (rows >= M hold zeros);
-          // lane j reads word (r, j) at 16B chunk (j/4) ^ (r&7): 32 distinct banks per row
-          const float* sf = reinterpret_cast<const float*>(stg);
-          float cs = 0.f;
-#pragma unroll
-          for (int r = 0; r < 32; ++r) cs += sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
-          if (n0 + lane < a.N) a.colsum[(int64_t)b * a.s_colsum + (int64_t)(mt * 4 + quad) * a.N + n0 + lane] = cs;
-        }
       }
       if (mn.prof) pacc[2] += clock64() - t_out0;
       if (EPI == EPI_RESID) {
@@ -688,28 +777,32 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
+    while (pend > 0) {  // the last parked tile
+      emit_group(p_next++);
+      --pend;
+    }
     if (lane == 0) bulk_wait0();
   }
   if (mn.prof && lane == 0) {
-    if (warp == 0) atomicAdd(&g_tcprof[mn.vid][P_TMA_EMPTY], pacc[0]);
-    if (warp == 1) {
+    if (warp == W_TMA_A) atomicAdd(&g_tcprof[mn.vid][P_TMA_EMPTY], pacc[0]);
+    if (warp == W_MMA) {
       atomicAdd(&g_tcprof[mn.vid][P_MMA_TEMPTY], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_MMA_FULLOP], pacc[1]);
       atomicAdd(&g_tcprof[mn.vid][P_MMA_ISSUE], pacc[2]);
     }
-    if (warp == 2) {
+    if (warp == W_CONV0) {
       atomicAdd(&g_tcprof[mn.vid][P_CONV_RAW], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_CONV_AFREE], pacc[1]);
       atomicAdd(&g_tcprof[mn.vid][P_CONV_B], pacc[2]);
     }
-    if (warp == 2 + NCONV + NEPI) atomicAdd(&g_tcprof[mn.vid][P_BTMA_EMPTY], pacc[0]);
-    if (warp == 2 + NCONV) {
+    if (warp == W_TMA_B) atomicAdd(&g_tcprof[mn.vid][P_BTMA_EMPTY], pacc[0]);
+    if (warp == W_EPI0) {
       atomicAdd(&g_tcprof[mn.vid][P_EPI_TFULL], pacc[0]); atomicAdd(&g_tcprof[mn.vid][P_EPI_XFULL], pacc[1]);
       atomicAdd(&g_tcprof[mn.vid][P_EPI_OUT], pacc[2]);
     }
-    if (warp == 0) atomicAdd(&g_tcprof[mn.vid][P_TOTAL], clock64() - t_k0);
+    if (warp == W_TMA_A) atomicAdd(&g_tcprof[mn.vid][P_TOTAL], clock64() - t_k0);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, 512);
+  if (warp == W_MMA) tmem_dealloc(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------------- host side ---

@@ -25,7 +25,11 @@ __global__ void k(int iters, unsigned long long* out) {
   __shared__ uint32_t holder;
   __shared__ __align__(8) uint64_t bar;
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) ((float*)base)[i] = 0.f;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+    unsigned h = (unsigned)i * 2654435761u ^ (blockIdx.x * 40503u);
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    ((float*)base)[i] = NOISE == 7 ? ((float)(h & 0xffffff) / 16777216.0f - 0.5f) : 0.f;
+  }
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&holder)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -39,32 +43,47 @@ __global__ void k(int iters, unsigned long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = holder;
+  if (NOISE == 7 && threadIdx.x < 128) {  // random A hi/lo columns 384..447 in TMEM
+    uint32_t r[32];
+    for (int i = 0; i < 32; ++i) r[i] = __float_as_uint((float)((threadIdx.x * 37 + i * 11) % 97) / 97.0f - 0.5f);
+    const uint32_t ta = tm + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16) + 384;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      :: "r"(ta), "r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5]),"r"(r[6]),"r"(r[7]),"r"(r[8]),"r"(r[9]),"r"(r[10]),"r"(r[11]),"r"(r[12]),"r"(r[13]),"r"(r[14]),"r"(r[15]),"r"(r[16]),"r"(r[17]),"r"(r[18]),"r"(r[19]),"r"(r[20]),"r"(r[21]),"r"(r[22]),"r"(r[23]),"r"(r[24]),"r"(r[25]),"r"(r[26]),"r"(r[27]),"r"(r[28]),"r"(r[29]),"r"(r[30]),"r"(r[31]) : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      :: "r"(ta + 32), "r"(r[0]),"r"(r[1]),"r"(r[2]),"r"(r[3]),"r"(r[4]),"r"(r[5]),"r"(r[6]),"r"(r[7]),"r"(r[8]),"r"(r[9]),"r"(r[10]),"r"(r[11]),"r"(r[12]),"r"(r[13]),"r"(r[14]),"r"(r[15]),"r"(r[16]),"r"(r[17]),"r"(r[18]),"r"(r[19]),"r"(r[20]),"r"(r[21]),"r"(r[22]),"r"(r[23]),"r"(r[24]),"r"(r[25]),"r"(r[26]),"r"(r[27]),"r"(r[28]),"r"(r[29]),"r"(r[30]),"r"(r[31]) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
   __shared__ volatile int stop;
   if (threadIdx.x == 0) stop = 0;
   __syncthreads();
-  if (NOISE == 5 && threadIdx.x >= 32) {
+  if ((NOISE == 5 || NOISE == 6) && threadIdx.x >= 32) {
     // bulk async copies global -> shared (the TMA engine) into a separate 16 KB region, 2 in flight
-    __shared__ __align__(8) uint64_t cb[2];
+    constexpr int NB = NOISE == 6 ? 6 : 2;
+    __shared__ __align__(8) uint64_t cb[6];
     if (threadIdx.x == 32) {
-      for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cb[i])));
+      for (int i = 0; i < NB; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cb[i])));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       unsigned long long n = 0;
-      uint32_t ph[2] = {0, 0};
+      uint32_t ph[6] = {0, 0, 0, 0, 0, 0};
       const char* src = (const char*)g_src + (size_t)blockIdx.x * 65536;
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < NB; ++i) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&cb[i])), "r"(8192) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(base + 49152 + i * 8192)), "l"(src + i * 8192), "r"(8192), "r"(su32(&cb[i])) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(base + 65536 + i * 8192)), "l"(src + i * 8192), "r"(8192), "r"(su32(&cb[i])) : "memory");
       }
       while (!stop) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NB; ++i) {
           asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W;}" ::"r"(su32(&cb[i])), "r"(ph[i]) : "memory");
           ph[i] ^= 1;
           ++n;
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&cb[i])), "r"(8192) : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(base + 49152 + i * 8192)), "l"(src + ((n & 7) * 8192)), "r"(8192), "r"(su32(&cb[i])) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(base + 65536 + i * 8192)), "l"(src + ((n & 7) * 8192)), "r"(8192), "r"(su32(&cb[i])) : "memory");
         }
       }
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < NB; ++i)
         asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @!P1 bra W;}" ::"r"(su32(&cb[i])), "r"(ph[i]) : "memory");
       out[148 + blockIdx.x] = n;
     }
@@ -141,20 +160,25 @@ template <int N, bool TS, int NOISE>
 void run(const char* name) {
   unsigned long long* d;
   cudaMalloc(&d, 2 * 148 * 8);
-  cudaFuncSetAttribute(k<N, TS, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  cudaFuncSetAttribute(k<N, TS, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000);
   const int iters = 20000;
-  k<N, TS, NOISE><<<148, NOISE >= 3 ? 288 : 128, 70000>>>(iters, d);
+  k<N, TS, NOISE><<<148, (NOISE >= 3 && NOISE != 7) ? 288 : 128, 140000>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[2 * 148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const double macs = (double)iters * 4 * 128 * N * 8;
-  const double lsu = NOISE == 5 ? (double)h[148] * 8192 / h[0] : NOISE >= 3 ? (double)h[148] * 8 * 4096 / h[0]
+  const double lsu = (NOISE == 5 || NOISE == 6) ? (double)h[148] * 8192 / h[0] : NOISE >= 3 ? (double)h[148] * 8 * 4096 / h[0]
                                  : (NOISE ? (double)h[148] * 96 * 16 * (NOISE > 1 ? 2 : 1) / h[0] : 0.0);
   printf("%s N=%d noise=%d: %.0f MAC/clk/SM (%.1f%% of 2048), LSU smem %.1f B/clk  %s\n", name, N, NOISE, macs / h[0],
          100.0 * macs / h[0] / 2048, lsu, cudaGetErrorString(e));
   cudaFree(d);
 }
 int main() {
+  run<128, true, 7>("ts-rand");
+  run<128, false, 7>("ss-rand");
+  run<256, false, 7>("ss-rand");
+  run<128, true, 6>("ts");
+  run<128, false, 6>("ss");
   run<128, true, 5>("ts");
   run<128, false, 5>("ss");
   run<256, false, 5>("ss");
