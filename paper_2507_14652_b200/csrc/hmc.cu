@@ -345,7 +345,7 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
   if (L.bias) { a.bias = x->Wd + L.b_off; a.s_bias = x->P; }
   if (L.act == ACT_SIN) { a.D = L.D; a.ldd = L.n_out; a.sD = L.rows * L.n_out; }
   PreSplit pre;
-  if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo + L.q_off; pre.ld = L.n_in; pre.stride = x->Ptc; }
+  if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc; }
   launch_gemm(x, a, true, true, st, "fwd", L.tc_w ? &pre : nullptr);
 }
 
@@ -411,7 +411,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.epi = EPI_DACT; a.act = Pv.act;
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
       PreSplit pre;
-      if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo + L.q_off; pre.ld = L.n_in; pre.stride = x->Ptc; }
+      if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc; }
       if (Pv.bias_active && N.colsum) { a.colsum = N.colsum; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
       N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
       cur ^= 1;
@@ -796,7 +796,9 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
   if (x->Ptc > 0) {
     x->Whi = dalloc<float>(x, (size_t)C * x->Ptc, err);
-    x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    // default: one raw fp32 plane, split in shared memory by the GEMM converters (half the L2
+    // traffic of pre-split hi/lo planes; the engine is bound by L2 -> SM bandwidth)
+    if (getenv("HMC_TC_PRESPLIT")) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
     x->d_tcpos = dalloc<int64_t>(x, x->k, err);
     CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 8, cudaMemcpyHostToDevice));
     for (auto& L : x->layers)

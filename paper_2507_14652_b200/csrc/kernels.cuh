@@ -24,7 +24,8 @@ struct KState {
   const float* inv_mass;       // nullptr = identity
   const uint32_t* chain_ids;
   float* Wd;                   // [C x P] dense per-chain parameters (frozen mu + active theta)
-  float* Whi; float* Wlo;      // [C x Ptc] tf32 hi / lo planes of the tensor-core layers' weights
+  float* Whi; float* Wlo;      // [C x Ptc] the tensor-core layers' weights: one raw plane (Wlo = nullptr)
+                               // or tf32 hi / lo planes; 16B-aligned rows for TMA
   const int64_t* tcpos;        // [k] position of active entry j in the planes, -1 if none
   int64_t Ptc;
   float* cur_theta; float* cur_grad; double* cur_logp;   // chain state (the cache)
@@ -47,9 +48,13 @@ __device__ __forceinline__ void put_param(const KState& s, int64_t c, int64_t j,
   if (s.tcpos) {
     const int64_t q = s.tcpos[j];
     if (q >= 0) {
-      const float h = tf32_hi(th);
-      s.Whi[c * s.Ptc + q] = h;
-      s.Wlo[c * s.Ptc + q] = th - h;
+      if (s.Wlo) {  // pre-split hi / lo planes
+        const float h = tf32_hi(th);
+        s.Whi[c * s.Ptc + q] = h;
+        s.Wlo[c * s.Ptc + q] = th - h;
+      } else {      // one raw plane (split in shared memory by the GEMM's converters)
+        s.Whi[c * s.Ptc + q] = th;
+      }
     }
   }
 }
@@ -72,9 +77,13 @@ __global__ void k_split_layer(const float* __restrict__ Wd, int64_t P, int64_t w
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = t / n, i = t - c * n;
     const float w = Wd[c * P + w_off + i];
-    const float h = tf32_hi(w);
-    Whi[c * Ptc + q_off + i] = h;
-    Wlo[c * Ptc + q_off + i] = w - h;
+    if (Wlo) {
+      const float h = tf32_hi(w);
+      Whi[c * Ptc + q_off + i] = h;
+      Wlo[c * Ptc + q_off + i] = w - h;
+    } else {
+      Whi[c * Ptc + q_off + i] = w;
+    }
   }
 }
 

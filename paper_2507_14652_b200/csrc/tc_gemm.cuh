@@ -256,6 +256,7 @@ struct MnDesc {
   int pf = 0;    // L2 prefetch distance of the TMA producer, in K blocks (0 = off)
   int prof = 0;  // accumulate per-role wait cycles into g_tcprof[vid]
   int vid = 0;   // kernel variant (index in tc_variants)
+  int dbg = 0;   // dev experiments: 1 = no MMAs, 2 = no converter work, 4 = no epilogue fold (results wrong)
 };
 
 // Instruction descriptor for kind::tf32 with fp32 accumulation.
@@ -437,6 +438,7 @@ __global__ void __launch_bounds__(NT, 1)
           const uint64_t dBl = dBh + (uint64_t)(C_::B_BYTES >> 4);
           const unsigned long long t_i0 = mn.prof ? clock64() : 0ull;
           if (elect_one()) {
+            if (!(mn.dbg & 1)) {
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               mma_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, kk == 0 ? 0u : 1u);
@@ -444,6 +446,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
+            }
             mma_commit(&b_empty[s]);
             mma_commit(&afree[jb % C_::NAS]);
             mma_commit(&tfull[buf]);
@@ -472,7 +475,10 @@ __global__ void __launch_bounds__(NT, 1)
         if (tlc) atomicMax(&g_tctl[6][jb], clock64());  // last converter warp has A
         const uint8_t* stA = sAr + sa * C_::A_BYTES;
         uint32_t hi[32], lo[32];
-        if (!A_MN) {  // row r: 8 x 16B chunks, chunk q at q ^ (r & 7) (128B swizzle)
+        if (mn.dbg & 2) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) { hi[k] = 0u; lo[k] = 0u; }
+        } else if (!A_MN) {  // row r: 8 x 16B chunks, chunk q at q ^ (r & 7) (128B swizzle)
           const float4* row = (const float4*)(stA + r * 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -498,8 +504,10 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t as = jb % C_::NAS;
         mbar_wait_t(&afree[as], ((jb / C_::NAS) & 1) ^ 1, mn.prof, pacc[1]);
         tc_fence_after();
-        tmem_st32(ta + as * 64, hi);
-        tmem_st32(ta + as * 64 + 32, lo);
+        if (!(mn.dbg & 2)) {
+          tmem_st32(ta + as * 64, hi);
+          tmem_st32(ta + as * 64 + 32, lo);
+        }
         if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
           uint8_t* stB = sBr + sb * C_::B_STAGE;
           mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
@@ -622,7 +630,7 @@ __global__ void __launch_bounds__(NT, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
-        for (int c0 = 0; c0 < NC; c0 += 32) {
+        for (int c0 = 0; c0 < ((mn.dbg & 4) ? 0 : NC); c0 += 32) {
           uint32_t r0[16], r1[16];
           tmem_ld16(taddr + c0, r0);
           tmem_ld16(taddr + c0 + 16, r1);
@@ -833,6 +841,7 @@ inline const TcVariant* tc_variants(int* n) {
 #define TV(AMN, BMN, PRE, EPI) {AMN, BMN, PRE, EPI, (TcKernel)tc::tc_gemm_kernel<BN, AMN, BMN, PRE, EPI>}
   static const TcVariant v[] = {
       TV(false, false, true, EPI_FWD),     // forward      Z = A W^T        (weights pre-split)
+      TV(false, false, false, EPI_FWD),    // forward, raw weight plane (split in shared memory)
       TV(false, true, true, EPI_DACT),     // input grad   G = (G W) o act'  (weights pre-split)
       TV(true, true, false, EPI_WGRAD),    // weight grad  dW = G^T A, compacted into the k-vector
       TV(false, false, false, EPI_RESID),  // DeepONet combine + residual
@@ -872,6 +881,7 @@ struct TcPlanner {
     encode = (tc::EncodeTiledFn)fn;
     if (const char* f = getenv("HMC_TC_PF")) mn.pf = std::max(0, atoi(f));
     if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
+    if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
@@ -900,6 +910,11 @@ struct TcPlanner {
     if (a.M < 64 || a.N < 32 || a.K < 32) return false;
     if (a.batch > 65535) return false;
     const bool amn = !akm, bmn = !bkm;
+    if (pre && !pre->lo) {  // raw weight plane: an ordinary B operand
+      GemmArgs b = a;
+      b.B = pre->hi; b.ldb = pre->ld; b.sB = pre->stride;
+      return accepts(b, akm, bkm, nullptr);
+    }
     if (!find(amn, bmn, pre != nullptr, a.epi)) return false;
     if (a.epi == EPI_FWD && a.act == ACT_SIN) return false;
     if ((a.lda % 4) || (a.sA % 4) || !al16(a.A) || (a.sA == 0 && a.batch > 1)) return false;
@@ -964,6 +979,11 @@ struct TcPlanner {
 
   // Returns false if a tensor map could not be encoded (caller falls back to SIMT).
   bool launch(const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const PreSplit* pre = nullptr) const {
+    if (pre && !pre->lo) {  // raw weight plane: an ordinary B operand
+      GemmArgs b = a;
+      b.B = pre->hi; b.ldb = pre->ld; b.sB = pre->stride;
+      return launch(b, akm, bkm, st, nullptr);
+    }
     const bool amn = !akm, bmn = !bkm;
     const TcVariant* v = find(amn, bmn, pre != nullptr, a.epi);
     if (!v) return false;
