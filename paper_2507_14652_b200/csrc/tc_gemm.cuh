@@ -83,7 +83,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+#ifndef TC_WAIT_MODE
+#define TC_WAIT_MODE 1
+#endif
+// TC_WAIT_MODE 0: try_wait with the default (system-dependent) suspend time;
+//              1: try_wait with a short suspend-time hint, so a sleeping waiter re-checks soon
+//                 after an async-proxy completion (tcgen05.commit / TMA complete_tx);
+//              2: test_wait spin (no suspension)
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#if TC_WAIT_MODE == 0
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -93,6 +101,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "}\n" ::"r"(su32(b)),
       "r"(parity)
       : "memory");
+#elif TC_WAIT_MODE == 1
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity), "r"(20)
+      : "memory");
+#else
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 // Optional per-role stall accounting (dev diagnostics, hmc_debug_tc_profile): cycles each role
 // spends waiting on each barrier, summed over CTAs.  Slots: see TcProf below.
@@ -138,6 +167,32 @@ __device__ __forceinline__ void tma_pf4(const CUtensorMap* m, int c0, int c1, in
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"((uint64_t)m),
                "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
+}
+// multicast variant: the box lands at the same shared offset in every CTA of ctaMask, each
+// CTA's barrier at `bar`'s offset receives the complete_tx
+__device__ __forceinline__ void tma_load3_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(su32(dst)),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                             int c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6], %7;" ::"r"(su32(dst)),
+      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // one lane of a converged warp returns true (elect.sync)
@@ -198,6 +253,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// commit arriving on the barrier at `bar`'s offset in every CTA of ctaMask
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   su32(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
@@ -323,7 +385,20 @@ __global__ void __launch_bounds__(NT, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
   const int tiles_per_b = n_mt * n_nt;
-  const int total = tiles_per_b * a.batch;
+  // CTA pairs (cluster of 2): the pair covers M tiles 2p and 2p+1 of the same (batch, N tile)
+  // and shares the B tile, each CTA TMA-multicasting one B plane to both
+  const uint32_t crank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int n_mp = (n_mt + 1) >> 1;
+  const int pairs_per_b = n_mp * n_nt;
+  const int total = pairs_per_b * a.batch;  // pair tiles
+  auto tile_of = [&](int t, int& b, int& mt, int& nt) {
+    b = t / pairs_per_b;
+    const int rem = t - b * pairs_per_b;
+    const int mp = rem / n_nt;
+    nt = rem - mp * n_nt;
+    mt = 2 * mp + (int)crank;
+  };
   const int nk = (a.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -333,7 +408,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
+      mbar_init(&b_empty[s], 2);  // both CTAs' MMAs release the (multicast-filled) stage
     }
     for (int i = 0; i < C_::NAS; ++i) {
       mbar_init(&full_op[i], NCONV * 32);
@@ -354,6 +429,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   unsigned long long pacc[3] = {0ull, 0ull, 0ull};
@@ -364,15 +440,18 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
-        const int mt = rem / n_nt;
+      for (int t = cid; t < total; t += ncl) {
+        int b, mt, nt;
+        tile_of(t, b, mt, nt);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait_t(&a_empty[s], ph ^ 1, mn.prof, pacc[0]);
           uint8_t* sA = sAr + s * C_::A_BYTES;
+          if (mn.dbg & 32) mbar_arrive(&a_full[s]);  // dev experiment: no A traffic
+          else {
           mbar_expect_tx(&a_full[s], C_::A_BYTES);
           if (A_MN) tma_load4(sA, &mA, &a_full[s], 0, kb * BK, mt * (BM / 32), b);
           else tma_load3(sA, &mA, &a_full[s], kb * BK, mt * BM, b);
+          }
           if (++s == SA) { s = 0; ph ^= 1; }
         }
       }
@@ -384,21 +463,25 @@ __global__ void __launch_bounds__(NT, 1)
       uint32_t ph = 0;
       const uint32_t bytes = (B_PRE ? 2 : 1) * C_::B_BYTES;
       uint32_t jq = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
-        const int nt = rem - (rem / n_nt) * n_nt;
+      for (int t = cid; t < total; t += ncl) {
+        int b, mt, nt;
+        tile_of(t, b, mt, nt);
         for (int kb = 0; kb < nk; ++kb, ++jq) {
           mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0]);
           if (mn.prof == 2 && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
+          // both CTAs of the pair receive the whole B stage: pre-split -> rank r loads plane r;
+          // raw -> rank 0 loads the plane; each multicast to the pair
+          if (mn.dbg & 16) mbar_arrive(&b_full[s]);  // dev experiment: no B traffic
+          else {
           mbar_expect_tx(&b_full[s], bytes);
-          if (B_MN) {
-            tma_load4(sBh, &mB, &b_full[s], 0, kb * BK, nt * (BN / 32), b);
-            if (B_PRE) tma_load4(sBl, &mB2, &b_full[s], 0, kb * BK, nt * (BN / 32), b);
-          } else {
-            tma_load3(sBh, &mB, &b_full[s], kb * BK, nt * BN, b);
-            if (B_PRE) tma_load3(sBl, &mB2, &b_full[s], kb * BK, nt * BN, b);
+          if (B_PRE || crank == 0) {
+            uint8_t* dst = (B_PRE && crank == 1) ? sBl : sBh;
+            const CUtensorMap* mp = (B_PRE && crank == 1) ? &mB2 : &mB;
+            if (B_MN) tma_load4_mc(dst, mp, &b_full[s], 0, kb * BK, nt * (BN / 32), b, (uint16_t)3);
+            else tma_load3_mc(dst, mp, &b_full[s], kb * BK, nt * BN, b, (uint16_t)3);
+          }
           }
           if (++s == SB) { s = 0; ph ^= 1; }
         }
@@ -420,7 +503,7 @@ __global__ void __launch_bounds__(NT, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t jb = 0;  // K blocks issued so far
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         for (int kb = 0; kb < nk; ++kb, ++jb) {
           const uint32_t buf = jb % NACC;
           const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
@@ -447,7 +530,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
             }
-            mma_commit(&b_empty[s]);
+            mma_commit_mc(&b_empty[s], (uint16_t)3);
             mma_commit(&afree[jb % C_::NAS]);
             mma_commit(&tfull[buf]);
           }
@@ -467,7 +550,7 @@ __global__ void __launch_bounds__(NT, 1)
     int sa = 0, sb = 0;
     uint32_t pha = 0, phb = 0;
     uint32_t jb = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = cid; t < total; t += ncl) {
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         // A first (the TMEM slot write is the long pole), then raw B planes if any
         mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0]);
@@ -553,6 +636,7 @@ __global__ void __launch_bounds__(NT, 1)
     // parked tile: pend groups left (emitted in order), its batch / row block / first column
     int pend = 0, p_next = 0, p_b = 0, p_m0 = 0, p_nb = 0, p_blk = 0, p_ng = 0;
     auto emit_group = [&](int g) {
+      if (mn.dbg & 8) return;  // dev experiment: no output traffic
       uint8_t* stg = stg0 + g * STG;
       float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
       const int n0 = p_nb + 32 * g;
@@ -578,7 +662,8 @@ __global__ void __launch_bounds__(NT, 1)
         float cs = 0.f;
 #pragma unroll
         for (int r = 0; r < 32; ++r) cs += sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
-        if (n0 + lane < a.N) a.colsum[(int64_t)p_b * a.s_colsum + (int64_t)p_blk * a.N + n0 + lane] = cs;
+        if (n0 + lane < a.N && p_blk * 32 < a.M)
+          a.colsum[(int64_t)p_b * a.s_colsum + (int64_t)p_blk * a.N + n0 + lane] = cs;
       }
     };
     // staging free for TMA loads / new parked tiles: all groups emitted and their stores have
@@ -603,9 +688,10 @@ __global__ void __launch_bounds__(NT, 1)
       __syncwarp();
     };
     uint32_t jb = 0, jt = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++jt) {
-      const int b = t / tiles_per_b, rem = t - b * tiles_per_b;
-      const int mt = rem / n_nt, nt = rem - mt * n_nt;
+    for (int t = cid; t < total; t += ncl, ++jt) {
+      int b, mt, nt;
+      tile_of(t, b, mt, nt);
+      const int rem = mt * n_nt + nt;  // tile index within the batch (residual partial slot)
       bool prefetched = false;
       if (loadx && pend == 0) {
         staging_free();
@@ -777,7 +863,7 @@ __global__ void __launch_bounds__(NT, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (lane == 0) { red[ew] = psq; red[NEPI + ew] = pr; }
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (ew == 0 && lane == 0) {
+        if (ew == 0 && lane == 0 && mt < n_mt) {
           double sq = 0.0, sr = 0.0;
           for (int w = 0; w < NEPI; ++w) { sq += red[w]; sr += red[NEPI + w]; }
           a.part_sq[(int64_t)b * a.n_part + rem] = sq;
@@ -810,6 +896,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still multicast into it or arrive on it
   if (warp == W_MMA) tmem_dealloc(tmem_base, 512);
 }
 
@@ -1008,12 +1095,25 @@ struct TcPlanner {
       ok = ok && map_store(&mX, const_cast<float*>(a.dsrc), a.M, a.N, a.ld_dsrc, a.s_dsrc, a.batch);
     if (a.epi == EPI_RESID) ok = ok && map_store(&mX, const_cast<float*>(a.V), a.M, a.N, a.ldv, 0, 1);
     if (!ok) return false;
-    const int tiles = ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN) * a.batch;
-    const int grid = tiles < num_sms ? tiles : num_sms;
+    const int pairs = (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch;
+    const int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
     int nv = 0;
     tc::MnDesc md = mn;
     md.vid = (int)(v - tc_variants<BN>(&nv));
-    v->fn<<<grid, tc::NT, tc::Cfg<BN>::SMEM, st>>>(mA, mB, mB2, mC, mX, a, md);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NT);
+    cfg.dynamicSmemBytes = tc::Cfg<BN>::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, v->fn, mA, mB, mB2, mC, mX, a, md) != cudaSuccess) return false;
     return true;
   }
 };
