@@ -404,19 +404,19 @@ __global__ void __launch_bounds__(NT, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_full[s], 1);
-      mbar_init(&a_empty[s], NCONV * 32);
+      mbar_init(&a_empty[s], NCONV);  // one arrive per converter warp
     }
     for (int s = 0; s < SB; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 2);  // both CTAs' MMAs release the (multicast-filled) stage
     }
     for (int i = 0; i < C_::NAS; ++i) {
-      mbar_init(&full_op[i], NCONV * 32);
+      mbar_init(&full_op[i], NCONV);
       mbar_init(&afree[i], 1);
     }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], NEPI * 32);
+      mbar_init(&tempty[i], NEPI);  // one arrive per epilogue warp
     }
     for (int i = 0; i < NEPI; ++i) mbar_init(&xfull[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -609,12 +609,17 @@ __global__ void __launch_bounds__(NT, 1)
         }
         // publish: A in TMEM (wait::st), B planes visible to the async proxy (the proxy fence
         // also orders this warp's raw-A reads before the A producer's next TMA write)
+        // (one elected arrive per warp after __syncwarp: per-thread arrives serialise on the
+        // SM's barrier unit and cost more than the whole K block of MMAs)
         tmem_wait_st();
         fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&full_op[as]);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&full_op[as]);
+          mbar_arrive(&a_empty[sa]);
+        }
         if (tlc) atomicMax(&g_tctl[7][jb], clock64());  // last converter warp published
-        mbar_arrive(&a_empty[sa]);
         if (++sa == SA) { sa = 0; pha ^= 1; }
         if (++sb == SB) { sb = 0; phb ^= 1; }
       }
@@ -728,7 +733,8 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[buf]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
         if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
         if (pend > 0) {  // one group of the parked tile per K block
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
