@@ -12,9 +12,11 @@ Plain, slow, obviously-correct NumPy float64 implementation of:
   philox.py   - Philox4x32-10 counter RNG, uniforms and Box-Muller normals
   hmc.py      - reduced-space log-posterior + gradient (Algorithm 2 target), momentum
                 draw, kick-drift-kick leapfrog, Metropolis-Hastings step, chains
+  sensitivity.py - parameter sensitivities S_i^2 (eqn:sensitivities) and the tau-partition
+                (eqn:threshold) of the step before the hot path
 
 Each function cites the PAPER.md passage (P:line) or SURVEY.md reading it follows.
 Parity status: every function is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
 (closed forms, finite differences, invariants, known answers); see DESIGN.md §4.
 """
-from . import network, philox, hmc  # noqa: F401
+from . import network, philox, hmc, sensitivity  # noqa: F401
