@@ -120,6 +120,17 @@ int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg,
  * grad [C x k] out.  In DATA mode every rank receives identical values. */
 int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream);
 
+/* Parameter sensitivities, the step before the hot path (Algorithm 2 "Compute: S_i^2",
+ * PAPER.md eqn:sensitivities P:193-197):  S_i^2 = sigma_i^2 / N_d * sum_j (dF_mu(x_j)/dtheta_i)^2
+ * for every flat parameter i (P = length of mu), gradients of the network OUTPUT at the VI mean
+ * mu.  MLP: N_d = n rows; DeepONet: N_d = n_c * n_x pairs (u_c, y_x).
+ * arch / data as for hmc_setup (data targets are not used); mu, sigma_vi [P] fp32 (host or
+ * device, sigma_vi >= 0); s2 [P] fp64 out (host or device).  Synchronous: returns when s2 is
+ * written.  Ranking and the tau threshold (eqn:threshold) are host logic on s2.
+ * HMC_E_CONFIG on invalid arguments (the same checks as hmc_setup), HMC_E_CUDA / HMC_E_OOM. */
+int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
+                    double* s2, void* stream);
+
 /* The dropped constant: -N log(sigma sqrt(2 pi)) - k log(sigma_p sqrt(2 pi)) (N = n_global or
  * n_c x n_x global), so logp + c is S:362's normalised value. */
 int hmc_logpost_const(const hmc_ctx* ctx, double* c);

@@ -54,7 +54,7 @@ class hmc_config(ctypes.Structure):
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
-           "hmc_debug_tc_profile", "hmc_debug_tc_timeline"]
+           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -254,6 +254,35 @@ def hmc_profile_read(ctx):
     recs = (hmc_prof_rec * max(n.value, 1))()
     _check(lib().hmc_profile_read(ctx, n.value, recs, ctypes.byref(n)), ctx)
     return [(r.name.decode(), r.ms, r.flops, r.bytes, r.step) for r in recs[:n.value]]
+
+
+def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):
+    """S_i^2 for every flat parameter (eqn:sensitivities) of problem.arch on problem's data, at
+    mu (default problem.frozen) with VI sds sigma_vi (default problem.sigma_vi).  Returns a
+    float64 NumPy array [P]."""
+    keep = []
+    arch = problem.arch
+    a = make_arch(arch.kind, [(n.widths, n.acts, n.bias) for n in arch.nets], arch.has_b0, keep)
+    d = hmc_data()
+    if arch.kind == "mlp":
+        d.x = _ptr(problem.x, keep, np.float32)
+        d.y = _ptr(problem.y, keep, np.float32)
+        d.n = int(problem.x.shape[0])
+    else:
+        d.u = _ptr(problem.u, keep, np.float32)
+        d.q = _ptr(problem.q, keep, np.float32)
+        d.v = _ptr(problem.v, keep, np.float32)
+        d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.q.shape[0])
+    mu = problem.frozen if mu is None else mu
+    sigma_vi = problem.sigma_vi if sigma_vi is None else sigma_vi
+    P = int(np.asarray(mu).shape[0]) if not hasattr(mu, "device") else int(mu.shape[0])
+    out = np.empty(P, dtype=np.float64)
+    L = lib()
+    L.hmc_sensitivity.argtypes = [ctypes.POINTER(hmc_arch), ctypes.POINTER(hmc_data), ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    _check(L.hmc_sensitivity(ctypes.byref(a), ctypes.byref(d), _ptr(mu, keep, np.float32),
+                             _ptr(sigma_vi, keep, np.float32), out.ctypes.data, _stream(stream)))
+    return out
 
 
 class Context:

@@ -43,6 +43,9 @@ struct GemmArgs {
   // EPI_DACT (tensor-core engine only): column sums of the output per 32-row block,
   // colsum[b * s_colsum + (m / 32) * N + n] (bias gradient of the layer below, fused)
   float* colsum; int64_t s_colsum;
+  // sensitivity mode (NEXT-1): EPI_WGRAD multiplies the SQUARED operands (sum_n G^2 X^2) and
+  // EPI_DACT's column partials sum the squared outputs
+  int sq;
 };
 
 template <int BM>
@@ -82,6 +85,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
       int m = A_KMAJOR ? la_m : la_m + e, kk = A_KMAJOR ? la_k + e : la_k;
       int gm = m0 + m, gk = kb + kk;
       ra[e] = (gm < a.M && gk < a.K) ? (A_KMAJOR ? A[(int64_t)gm * a.lda + gk] : A[(int64_t)gk * a.lda + gm]) : 0.f;
+      if (a.sq && a.epi == EPI_WGRAD) ra[e] *= ra[e];
       int n = B_KMAJOR ? lb_n : lb_n + e, kn = B_KMAJOR ? lb_k + e : lb_k;
       int gn = n0 + n, gkn = kb + kn;
       float v = 0.f;
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a) {
         if (gn == a.ones_col) v = 1.f;
         else v = B_KMAJOR ? B[(int64_t)gn * a.ldb + gkn] : B[(int64_t)gkn * a.ldb + gn];
       }
-      rb[e] = v;
+      rb[e] = (a.sq && a.epi == EPI_WGRAD) ? v * v : v;
     }
   };
   auto store = [&](int buf) {

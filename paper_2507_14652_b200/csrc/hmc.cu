@@ -93,6 +93,7 @@ struct hmc_ctx {
   float* R = nullptr;
   float* colred = nullptr;
   float* narrow_part = nullptr;  // pass-1 partials of the narrow-input weight gradients
+  int sq = 0;                    // sensitivity mode (hmc_sensitivity): squared weight-gradient sums
   int colred_chunks = 0;
   double* d_eps = nullptr;
   Rec* d_rec = nullptr;
@@ -268,8 +269,10 @@ void prof_end(hmc_ctx* x, int id, cudaStream_t st, const std::string& name, doub
 }
 
 // returns true if the tensor-core engine ran it
-bool launch_gemm(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag,
+bool launch_gemm(hmc_ctx* x, const GemmArgs& a_in, bool akm, bool bkm, cudaStream_t st, const char* tag,
                  const PreSplit* pre = nullptr) {
+  GemmArgs a = a_in;
+  a.sq = x->sq;
   const int id = prof_begin(x, st);
   bool tc = x->tc.accepts(a, akm, bkm, pre);
   if (tc) tc = x->tc.launch(a, akm, bkm, st, pre);
@@ -304,7 +307,7 @@ void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const f
                          cudaStream_t st) {
   const int nch = (int)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS);
   dim3 grid(nch, x->C);
-#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->narrow_part, nch)
+#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->narrow_part, nch, x->sq)
   switch (L.n_in) {
     case 1: WN(1); break; case 2: WN(2); break; case 3: WN(3); break; case 4: WN(4); break;
     case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;
@@ -367,6 +370,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
       a.B = in; a.ldb = L.n_in; a.sB = s_in;
       a.epi = EPI_WGRAD;
+      a.sq = x->sq;
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       const int id = prof_begin(x, st);
@@ -387,7 +391,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
             k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
-                                                             x->colred, chunks);
+                                                             x->colred, chunks, x->sq);
             k_colred_p2<<<x->C, 256, 0, st>>>(x->colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
                                               x->k);
             x->launches += 2;
@@ -439,10 +443,14 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
       x->flop_acc += 2.0 * C * O.rows * O.n_in;
       prof_end(x, id, st, "out_fwd", 2.0 * C * O.rows * O.n_in, 4.0 * C * O.rows * (O.n_in + 1));
     }
+    if (x->sq) {  // sensitivity mode: dF/dF = 1 for every datum (output seed, no residual)
+      k_fill<<<148 * 4, 256, 0, st>>>(x->R, (int64_t)C * O.rows, 1.f);
+      x->launches++;
+    }
     if (N.l_min < 0) return;
     if (O.any_active) {
       dim3 g1(x->colred_chunks, C);
-      k_colred_p1<<<g1, 256, 0, st>>>(x->R, in, s_in, O.rows, O.n_in, x->colred, x->colred_chunks);
+      k_colred_p1<<<g1, 256, 0, st>>>(x->R, in, s_in, O.rows, O.n_in, x->colred, x->colred_chunks, x->sq);
       k_colred_p2<<<C, 256, 0, st>>>(x->colred, x->colred_chunks, O.n_in, x->d_slot + O.w_off,
                                      O.bias ? x->d_slot + O.b_off : nullptr, x->gl, x->k);
       x->launches += 2;
@@ -532,6 +540,110 @@ void enqueue_step(hmc_ctx* x, int mode, cudaStream_t st, std::string& err) {
   }
   x->launches++;
   prof_end(x, idf, st, "finalize", 0.0, 0.0);
+}
+
+// ---- sensitivity step (eqn:sensitivities P:193-197) ----
+// Symmetric eigen-decomposition by cyclic Jacobi rotations (host, fp64): A (n x n, row-major,
+// destroyed) -> eigenvalues w[n], eigenvectors as the columns of V.  Used on the p x p output
+// Gram matrices of the DeepONet branch / trunk (p <= 256).
+void jacobi_eig(std::vector<double>& A, int n, std::vector<double>& w, std::vector<double>& V) {
+  V.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) (i == j ? diag : off) += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+    if (off <= 1e-30 * (diag + 1e-300)) break;
+    for (int pp = 0; pp < n - 1; ++pp)
+      for (int q = pp + 1; q < n; ++q) {
+        const double apq = A[(size_t)pp * n + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double app = A[(size_t)pp * n + pp], aqq = A[(size_t)q * n + q];
+        const double th = 0.5 * (aqq - app) / apq;
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {  // rotate columns pp, q
+          const double akp = A[(size_t)k * n + pp], akq = A[(size_t)k * n + q];
+          A[(size_t)k * n + pp] = c * akp - sn * akq;
+          A[(size_t)k * n + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // rotate rows pp, q
+          const double apk = A[(size_t)pp * n + k], aqk = A[(size_t)q * n + k];
+          A[(size_t)pp * n + k] = c * apk - sn * aqk;
+          A[(size_t)q * n + k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[(size_t)k * n + pp], vkq = V[(size_t)k * n + q];
+          V[(size_t)k * n + pp] = c * vkp - sn * vkq;
+          V[(size_t)k * n + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  w.resize(n);
+  for (int i = 0; i < n; ++i) w[i] = A[(size_t)i * n + i];
+}
+
+// Seeds s_m = sqrt(lambda_m) v_m of G = X^T X (X: rows x p, chain 0 of a net's output), so
+// that sum_m (s_m . g)^2 = g^T G g for any g (negative rounding eigenvalues clipped to 0)
+std::vector<float> gram_seeds(const std::vector<float>& X, int64_t rows, int p) {
+  std::vector<double> G((size_t)p * p, 0.0);
+  for (int64_t r = 0; r < rows; ++r)
+    for (int i = 0; i < p; ++i) {
+      const double xi = X[(size_t)r * p + i];
+      if (xi == 0.0) continue;
+      for (int j = 0; j < p; ++j) G[(size_t)i * p + j] += xi * (double)X[(size_t)r * p + j];
+    }
+  std::vector<double> w, V;
+  jacobi_eig(G, p, w, V);
+  std::vector<float> seeds((size_t)p * p);
+  for (int m = 0; m < p; ++m) {
+    const double sl = std::sqrt(std::max(w[m], 0.0));
+    for (int k = 0; k < p; ++k) seeds[(size_t)m * p + k] = (float)(sl * V[(size_t)k * p + m]);
+  }
+  return seeds;
+}
+
+// Sum over data of the squared output gradients, for every parameter and virtual chain, into
+// x->gl [C x P] (x was set up with k = P, theta = mu).  MLP: one chain, output seed 1 per
+// datum.  DeepONet: chain m seeds the branch with sqrt(l_m) v_m of the trunk Gram matrix and
+// the trunk with those of the branch Gram matrix, since sum_x (dF(c,x)/dtheta_branch)^2 =
+// g_c^T (T^T T) g_c with g_c = dB(c)/dtheta (and symmetrically for the trunk).
+void enqueue_sensitivity(hmc_ctx* x, std::string& err) {
+  cudaStream_t st = x->st;
+  x->sq = 1;
+  if (x->kind == HMC_MLP) {
+    enqueue_body(x, st);
+    return;
+  }
+  for (int ni = 0; ni < 2; ++ni) {
+    NetInfo& N = x->nets[ni];
+    for (int i = 0; i < (int)N.layers.size(); ++i) enqueue_forward_hidden(x, N, i, st);
+  }
+  NetInfo& Nb = x->nets[0];
+  NetInfo& Nt = x->nets[1];
+  const LayerInfo& Bl = x->layers[Nb.layers.back()];
+  const LayerInfo& Tl = x->layers[Nt.layers.back()];
+  const int p = Bl.n_out;
+  std::vector<float> hB((size_t)x->n_c * p), hT((size_t)x->n_x * p);
+  CK(cudaMemcpyAsync(hB.data(), Bl.A, hB.size() * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hT.data(), Tl.A, hT.size() * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const std::vector<float> sT = gram_seeds(hT, x->n_x, p);  // seeds of the branch reverse pass
+  const std::vector<float> sB = gram_seeds(hB, x->n_c, p);  // seeds of the trunk reverse pass
+  float* dseed = dalloc<float>(x, (size_t)2 * p * p, err);
+  CK(cudaMemcpyAsync(dseed, sT.data(), sT.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dseed + (size_t)p * p, sB.data(), sB.size() * 4, cudaMemcpyHostToDevice, st));
+  if (Nb.l_min >= 0) {
+    k_seed_top<<<148 * 4, 256, 0, st>>>(Bl.A, Bl.D, Bl.act, dseed, x->n_c, p, x->C, Nb.G[0]);
+    Nb.cs_ready = false;
+    enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+  }
+  if (Nt.l_min >= 0) {
+    k_seed_top<<<148 * 4, 256, 0, st>>>(Tl.A, Tl.D, Tl.act, dseed + (size_t)p * p, x->n_x, p, x->C, Nt.G[0]);
+    Nt.cs_ready = false;
+    enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+  }
+  CK(cudaGetLastError());
 }
 
 void capture_begin(hmc_ctx* x, std::string& err) {
@@ -1042,6 +1154,60 @@ int hmc_trajectory(hmc_ctx* ctx, float* theta, double* logp, float* grad, double
 int hmc_sample(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
                int32_t S, float* samples, uint8_t* acc, double* dH, void* stream) {
   return run_traj(ctx, theta, logp, grad, eps, L, iter0, S, samples, acc, dH, stream);
+}
+
+int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
+                    double* s2, void* stream) {
+  if (!arch || !data || !mu || !sigma_vi || !s2) {
+    g_err = "config: arch, data, mu, sigma_vi and s2 must be non-NULL";
+    return HMC_E_CONFIG;
+  }
+  std::unique_ptr<hmc_ctx> x(new hmc_ctx());
+  std::string& err = x->err;
+  try {
+    // P from the architecture (the same walk setup_impl validates)
+    int64_t P = 0;
+    for (int ni = 0; ni < (arch->kind == HMC_DEEPONET ? 2 : 1); ++ni) {
+      const hmc_net& nt = arch->net[ni];
+      CFG(nt.n_layers >= 1 && nt.widths && nt.acts && nt.has_bias, "net description incomplete");
+      for (int l = 0; l < nt.n_layers; ++l)
+        P += (int64_t)nt.widths[l] * nt.widths[l + 1] + (nt.has_bias[l] ? nt.widths[l + 1] : 0);
+    }
+    if (arch->kind == HMC_DEEPONET && arch->has_b0) P += 1;
+    std::vector<int32_t> idx((size_t)P);
+    for (int64_t j = 0; j < P; ++j) idx[j] = (int32_t)j;
+    const std::vector<float> hmu = to_host(mu, (size_t)P, err);
+    const std::vector<float> hsig = to_host(sigma_vi, (size_t)P, err);
+    for (float v : hsig) CFG(std::isfinite(v) && v >= 0.f, "sigma_vi must be finite and >= 0");
+    const int p = arch->kind == HMC_DEEPONET ? arch->net[0].widths[arch->net[0].n_layers] : 1;
+    CFG(arch->kind != HMC_DEEPONET || p <= 1024, "DeepONet output width > 1024");
+    hmc_config cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.frozen = hmu.data();
+    cfg.idx = idx.data();
+    cfg.P = P;
+    cfg.k = P;
+    cfg.noise_sigma = 1.0;
+    cfg.prior_sigma = 1.0;
+    cfg.n_chains = arch->kind == HMC_DEEPONET ? p : 1;
+    cfg.mode = HMC_MODE_SINGLE;
+    cfg.world = 1;
+    setup_impl(x.get(), arch, data, &cfg, err);
+    enqueue_sensitivity(x.get(), err);
+    float* dsig = dalloc<float>(x.get(), (size_t)P, err);
+    double* dout = dalloc<double>(x.get(), (size_t)P, err);
+    CK(cudaMemcpyAsync(dsig, hsig.data(), (size_t)P * 4, cudaMemcpyHostToDevice, x->st));
+    const double n_d = x->kind == HMC_MLP ? (double)x->n : (double)x->n_c * (double)x->n_x;
+    k_sens_finalize<<<148 * 4, 256, 0, x->st>>>(x->gl, x->C, P, dsig, n_d, x->has_b0 ? x->b0_off : -1, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s2, dout, (size_t)P * 8, cudaMemcpyDefault, x->st));
+    CK(cudaStreamSynchronize(x->st));
+    (void)stream;
+  } catch (Fail f) {
+    g_err = err;
+    return f.code;
+  }
+  return HMC_OK;
 }
 
 int hmc_destroy(hmc_ctx* ctx) {

@@ -142,7 +142,7 @@ __global__ void k_rank1_dact(const float* __restrict__ R, const float* __restric
 //      part[c][chunk][j] = sum_n R[n] X[n, j] (j < n_in), and sum_n R[n] at j = n_in ----
 constexpr int COLRED_CH = 256;
 __global__ void k_colred_p1(const float* __restrict__ R, const float* __restrict__ X, int64_t sX,
-                            int64_t rows, int n_in, float* __restrict__ part, int n_chunks) {
+                            int64_t rows, int n_in, float* __restrict__ part, int n_chunks, int sq = 0) {
   const int c = blockIdx.y, ch = blockIdx.x;
   const float* Xc = X + (int64_t)c * sX;
   const float* Rc = R ? R + (int64_t)c * rows : nullptr;
@@ -151,10 +151,15 @@ __global__ void k_colred_p1(const float* __restrict__ R, const float* __restrict
   for (int j = threadIdx.x; j <= n_in; j += blockDim.x) {
     float s = 0.f;
     if (j < n_in) {
-      if (R) for (int64_t n = n0; n < n1; ++n) s = fmaf(Rc[n], Xc[n * n_in + j], s);
+      if (sq) {  // sensitivity mode: sum R^2 X^2 (sum X^2 without R)
+        for (int64_t n = n0; n < n1; ++n) {
+          const float xv = Xc[n * n_in + j], rv = R ? Rc[n] : 1.f;
+          s = fmaf(rv * rv, xv * xv, s);
+        }
+      } else if (R) for (int64_t n = n0; n < n1; ++n) s = fmaf(Rc[n], Xc[n * n_in + j], s);
       else for (int64_t n = n0; n < n1; ++n) s += Xc[n * n_in + j];
     } else if (R) {
-      for (int64_t n = n0; n < n1; ++n) s += Rc[n];
+      for (int64_t n = n0; n < n1; ++n) s += sq ? Rc[n] * Rc[n] : Rc[n];
     }
     part[((int64_t)c * n_chunks + ch) * (n_in + 1) + j] = s;
   }
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X,
 template <int DIN>
 __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict__ G, int64_t sG, const float* __restrict__ X,
                                                          int64_t sX, int64_t rows, int n_out, float* __restrict__ part,
-                                                         int n_chunks) {
+                                                         int n_chunks, int sq) {
   __shared__ float xs[NARROW_ROWS * DIN];
   const int c = blockIdx.y, ch = blockIdx.x;
   const int64_t r0 = (int64_t)ch * NARROW_ROWS;
@@ -230,9 +235,13 @@ __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict
     for (int i = 0; i <= DIN; ++i) acc[i] = 0.f;
     const float* g = G + (int64_t)c * sG + r0 * n_out + o;
     for (int r = 0; r < nr; ++r) {
-      const float gv = g[(int64_t)r * n_out];
+      float gv = g[(int64_t)r * n_out];
+      if (sq) gv *= gv;   // sensitivity mode: sum G^2 X^2 and sum G^2
 #pragma unroll
-      for (int i = 0; i < DIN; ++i) acc[i] = fmaf(gv, xs[r * DIN + i], acc[i]);
+      for (int i = 0; i < DIN; ++i) {
+        const float xv = xs[r * DIN + i];
+        acc[i] = fmaf(gv, sq ? xv * xv : xv, acc[i]);
+      }
       acc[DIN] += gv;
     }
     float* pp = part + (((int64_t)c * n_chunks + ch) * n_out + o) * (DIN + 1);
@@ -254,6 +263,39 @@ __global__ void k_wgrad_narrow_p2(const float* __restrict__ part, int n_chunks, 
     float acc = 0.f;
     for (int ch = 0; ch < n_chunks; ++ch) acc += part[((int64_t)c * n_chunks + ch) * per + t];
     gl[(int64_t)c * k + sl] = acc;
+  }
+}
+
+// ---- sensitivity step (NEXT-1, eqn:sensitivities P:193-197) ----
+__global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    p[t] = v;
+}
+
+// DeepONet output seeds: G[m][r][k] = seed[m][k] * act'(output_k of row r) (the reverse pass
+// of seed . B (or seed . T) through the net's top layer, one seed vector per virtual chain m)
+__global__ void k_seed_top(const float* __restrict__ A, const float* __restrict__ D, int act,
+                           const float* __restrict__ seed, int64_t rows, int p, int C, float* __restrict__ G) {
+  const int64_t per = rows * p, total = per * C;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = t / per, k = t % p;
+    float v = seed[m * p + k];
+    if (act == ACT_TANH) { const float a = A[t]; v *= (1.f - a * a); }
+    else if (act == ACT_SIN) v *= D[t];
+    G[t] = v;
+  }
+}
+
+// S2[j] = sigma_j^2 * (sum_m sumsq[m][j]) / N_d in fp64, chains summed in fixed order
+__global__ void k_sens_finalize(const float* __restrict__ sumsq, int C, int64_t P, const float* __restrict__ sigma,
+                                double n_d, int64_t b0, double* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (j == b0) s = n_d;  // dF/db0 = 1 for every pair
+    else
+      for (int m = 0; m < C; ++m) s += (double)sumsq[(int64_t)m * P + j];
+    const double sg = (double)sigma[j];
+    out[j] = sg * sg * s / n_d;
   }
 }
 

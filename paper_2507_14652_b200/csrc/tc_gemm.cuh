@@ -565,7 +565,8 @@ __global__ void __launch_bounds__(NT, 1)
           const float4* row = (const float4*)(stA + r * 128);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float4 x = row[q ^ (r & 7)];
+            float4 x = row[q ^ (r & 7)];
+            if (EPI == EPI_WGRAD && a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
             const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -578,7 +579,8 @@ __global__ void __launch_bounds__(NT, 1)
           const float* col = (const float*)stA + (r >> 5) * 1024 + (r & 31);
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float x = col[k * 32];
+            float x = col[k * 32];
+            if (EPI == EPI_WGRAD && a.sq) x *= x;
             const float h = tf32_rna(x);
             hi[k] = __float_as_uint(h);
             lo[k] = __float_as_uint(x - h);
@@ -599,7 +601,8 @@ __global__ void __launch_bounds__(NT, 1)
           float4* bl = (float4*)(stB + C_::B_BYTES);
 #pragma unroll 4
           for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
-            const float4 x = bh[i];
+            float4 x = bh[i];
+            if (EPI == EPI_WGRAD && a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
             float4 h, l;
             h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
             l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
@@ -666,7 +669,10 @@ __global__ void __launch_bounds__(NT, 1)
         const float* sf = reinterpret_cast<const float*>(stg);
         float cs = 0.f;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) cs += sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
+        for (int r = 0; r < 32; ++r) {
+          const float v = sf[r * 32 + ((((lane >> 2) ^ (r & 7)) << 2) | (lane & 3))];
+          cs += a.sq ? v * v : v;
+        }
         if (n0 + lane < a.N && p_blk * 32 < a.M)
           a.colsum[(int64_t)p_b * a.s_colsum + (int64_t)p_blk * a.N + n0 + lane] = cs;
       }
