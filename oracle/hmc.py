@@ -134,3 +134,58 @@ def sample_chain(target, theta0, eps, L, iter0, S, chain):
         acc[s] = r["accepted"]
         dHs[s] = r["dH"]
     return samples, acc, dHs
+
+
+# ---- step-size adaptation ----
+# "the step size is computed using the step size adaptation method proposed in
+# Algorithm 5 of [Hoffman & Gelman]" with the acceptance rate fixed at 80 %.  Dual averaging:
+#   mu = log(10 eps0), Hbar_0 = 0, log epsbar_0 = 0, gamma = 0.05, t0 = 10, kappa = 0.75;
+#   after adaptation trajectory m (run with eps_{m-1}) with acceptance statistic
+#   alpha_m = min(1, exp(H0 - H*)) (0 for a non-finite H*):
+#     Hbar_m = (1 - 1/(m + t0)) Hbar_{m-1} + (delta - alpha_m) / (m + t0)
+#     log eps_m = mu - sqrt(m) / gamma * Hbar_m
+#     log epsbar_m = m^-kappa log eps_m + (1 - m^-kappa) log epsbar_{m-1}
+#   and sampling after adaptation uses epsbar_M.
+DA_GAMMA, DA_T0, DA_KAPPA = 0.05, 10.0, 0.75
+
+
+def accept_stat(H0, H1):
+    """alpha = min(1, exp(H0 - H*)), 0 when H* is not finite (the proposal is rejected)."""
+    if not np.isfinite(H1):
+        return 0.0
+    d = H0 - H1
+    return 1.0 if d >= 0 else math.exp(d)
+
+
+def da_init(eps0):
+    return {"mu": math.log(10.0 * eps0), "hbar": 0.0, "log_epsbar": 0.0, "m": 0, "log_eps": math.log(eps0)}
+
+
+def da_update(st, alpha, delta):
+    """One dual-averaging step (Algorithm 5 of Hoffman & Gelman, quoted above)."""
+    m = st["m"] + 1
+    eta = 1.0 / (m + DA_T0)
+    hbar = (1.0 - eta) * st["hbar"] + eta * (delta - alpha)
+    log_eps = st["mu"] - math.sqrt(m) / DA_GAMMA * hbar
+    w = m ** (-DA_KAPPA)
+    log_epsbar = w * log_eps + (1.0 - w) * st["log_epsbar"]
+    return {"mu": st["mu"], "hbar": hbar, "log_epsbar": log_epsbar, "m": m, "log_eps": log_eps}
+
+
+def adapt_chain(target, theta0, eps0, L, iter0, n_adapt, delta, chain):
+    """n_adapt adaptation trajectories of one chain (warm-up; the state advances as in
+    sampling).  Returns (epsbar, per-trajectory eps used, accept flags, alphas, final state)."""
+    theta = np.asarray(theta0, dtype=np.float64)
+    lp, g = target.logp_grad(theta)
+    st = da_init(eps0)
+    eps_used, accs, alphas = [], [], []
+    for s in range(n_adapt):
+        eps = math.exp(st["log_eps"])
+        r = trajectory(target, theta, lp, g, eps, L, iter0 + s, chain)
+        theta, lp, g = r["theta"], r["logp"], r["grad"]
+        a = accept_stat(r["H0"], r["H1"])
+        st = da_update(st, a, delta)
+        eps_used.append(eps)
+        accs.append(r["accepted"])
+        alphas.append(a)
+    return math.exp(st["log_epsbar"]), np.array(eps_used), np.array(accs), np.array(alphas), (theta, lp, g)
