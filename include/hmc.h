@@ -120,6 +120,18 @@ int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg,
  * grad [C x k] out.  In DATA mode every rank receives identical values. */
 int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream);
 
+/* Step-size adaptation ("the acceptance rate ... is fixed
+ * at 80 % and the step size is computed using ... Algorithm 5 of" Hoffman & Gelman): n_adapt
+ * trajectories (warm-up: the chain state theta / logp / grad advances exactly as in hmc_sample,
+ * iter0 .. iter0 + n_adapt - 1), each chain running dual averaging on its own step size from
+ * eps0 towards the acceptance statistic delta (gamma 0.05, t0 10, kappa 0.75; alpha =
+ * min(1, exp(H0 - H*)), 0 for non-finite H*).  eps_bar [C] (host or device, fp64) receives
+ * each chain's averaged step; the context keeps them, and hmc_trajectory / hmc_sample with
+ * eps == 0 then use them per chain.  acc / dH [C x n_adapt] optional as in hmc_sample.
+ * HMC_E_CONFIG if eps0 <= 0, delta outside (0, 1), n_adapt < 1. */
+int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0, int32_t L, int64_t iter0,
+              int32_t n_adapt, double delta, double* eps_bar, uint8_t* acc, double* dH, void* stream);
+
 /* Parameter sensitivities, the step before the hot path (Algorithm 2 "Compute: S_i^2",
  * PAPER.md eqn:sensitivities P:193-197):  S_i^2 = sigma_i^2 / N_d * sum_j (dF_mu(x_j)/dtheta_i)^2
  * for every flat parameter i (P = length of mu), gradients of the network OUTPUT at the VI mean
@@ -140,8 +152,8 @@ int hmc_logpost_const(const hmc_ctx* ctx, double* c);
  * start gradient taken from `grad` (the cache), Metropolis test with u from Philox tag 1.
  * theta[C x k], logp[C], grad[C x k] are in/out: on accept they become the proposal's, on
  * reject they are unchanged.  acc[C] (0/1) and dH[C] = H* - H0 are outputs (either may be NULL).
- * L = 0 is the identity and always accepts.  eps must be finite and > 0, L >= 0,
- * 0 <= iter < 2^32. */
+ * L = 0 is the identity and always accepts.  eps must be finite and > 0 (or 0 after
+ * hmc_adapt: each chain then uses its adapted step), L >= 0, 0 <= iter < 2^32. */
 int hmc_trajectory(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L,
                    int64_t iter, uint8_t* acc, double* dH, void* stream);
 

@@ -54,7 +54,7 @@ class hmc_config(ctypes.Structure):
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
-           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity"]
+           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -254,6 +254,21 @@ def hmc_profile_read(ctx):
     recs = (hmc_prof_rec * max(n.value, 1))()
     _check(lib().hmc_profile_read(ctx, n.value, recs, ctypes.byref(n)), ctx)
     return [(r.name.decode(), r.ms, r.flops, r.bytes, r.step) for r in recs[:n.value]]
+
+
+def hmc_adapt(ctx, theta, logp, grad, eps0, L, iter0, n_adapt, delta, acc=None, dH=None, stream=None):
+    """Dual-averaging warm-up (include/hmc.h hmc_adapt); returns the per-chain eps_bar (NumPy)."""
+    keep = []
+    L_ = lib()
+    L_.hmc_adapt.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                             ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    C = int(theta.shape[0])
+    out = np.empty(C, dtype=np.float64)
+    _check(L_.hmc_adapt(ctx, _ptr(theta, keep, np.float32), _ptr(logp, keep, np.float64), _ptr(grad, keep, np.float32),
+                        float(eps0), int(L), int(iter0), int(n_adapt), float(delta), out.ctypes.data,
+                        _ptr(acc, keep, np.uint8), _ptr(dH, keep, np.float64), _stream(stream)), ctx)
+    return out
 
 
 def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):

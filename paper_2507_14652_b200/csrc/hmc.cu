@@ -95,7 +95,9 @@ struct hmc_ctx {
   float* narrow_part = nullptr;  // pass-1 partials of the narrow-input weight gradients
   int sq = 0;                    // sensitivity mode (hmc_sensitivity): squared weight-gradient sums
   int colred_chunks = 0;
-  double* d_eps = nullptr;
+  double* d_eps = nullptr;   // [C] per-chain step sizes
+  double* d_da = nullptr;    // [C x 4] dual-averaging state (NEXT-2)
+  bool adapted = false;      // per-chain epsbar from hmc_adapt in d_eps
   Rec* d_rec = nullptr;
   uint8_t* tmp_acc = nullptr;
   double* tmp_dH = nullptr;
@@ -141,7 +143,7 @@ struct hmc_ctx {
     s.Wd = Wd; s.Whi = Whi; s.Wlo = Wlo; s.tcpos = d_tcpos; s.Ptc = Ptc; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
     s.wrk_theta = wrk_theta; s.wrk_grad = wrk_grad; s.wrk_logp = wrk_logp; s.p = p; s.H0 = H0;
     s.gl = gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
-    s.eps = d_eps; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
+    s.eps = d_eps; s.da = d_da; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
     return s;
   }
   ~hmc_ctx() {
@@ -741,8 +743,9 @@ void cpy(void* dst, const void* src, size_t bytes, cudaStream_t st, std::string&
   if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
 }
 
+// eps > 0: every chain uses eps; eps == 0: the per-chain values already in d_eps (hmc_adapt)
 void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, int64_t iter, double eps,
-             std::string& err) {
+             std::string& err, int adapt = 0, double delta = 0.0) {
   CK(cudaEventSynchronize(x->ev_stage));  // previous staging copy consumed
   x->h_rec->samples = samples;
   x->h_rec->acc = acc;
@@ -750,9 +753,10 @@ void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, in
   x->h_rec->S = S;
   x->h_rec->sidx = 0;
   x->h_rec->iter = iter;
-  *x->h_eps = eps;
+  x->h_rec->adapt = adapt;
+  x->h_rec->delta = delta;
   CK(cudaMemcpyAsync(x->d_rec, x->h_rec, sizeof(Rec), cudaMemcpyHostToDevice, x->st));
-  CK(cudaMemcpyAsync(x->d_eps, x->h_eps, sizeof(double), cudaMemcpyHostToDevice, x->st));
+  if (eps > 0) k_fill_d<<<1, 256, 0, x->st>>>(x->d_eps, x->C, eps);
   CK(cudaEventRecord(x->ev_stage, x->st));
 }
 
@@ -930,7 +934,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   x->wrk_logp = dalloc<double>(x, C, err);
   x->H0 = dalloc<double>(x, C, err);
   x->lik = dalloc<double>(x, C, err);
-  x->d_eps = dalloc<double>(x, 1, err);
+  x->d_eps = dalloc<double>(x, C, err);
+  x->d_da = dalloc<double>(x, (size_t)4 * C, err);
   x->d_rec = dalloc<Rec>(x, 1, err);
   x->tmp_acc = dalloc<uint8_t>(x, C, err);
   x->tmp_dH = dalloc<double>(x, C, err);
@@ -1096,10 +1101,13 @@ int hmc_logpost_const(const hmc_ctx* ctx, double* c) {
 }
 
 static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
-                    int32_t S, float* samples, uint8_t* acc, double* dH, void* stream) {
+                    int32_t S, float* samples, uint8_t* acc, double* dH, void* stream, int adapt = 0,
+                    double delta = 0.0, double* eps_bar = nullptr) {
   API_BEGIN(ctx)
   CFG(theta && logp && grad, "theta, logp and grad must be non-NULL");
-  CFG(std::isfinite(eps) && eps > 0, "eps must be finite and > 0");
+  CFG(std::isfinite(eps) && (eps > 0 || (eps == 0 && ctx->adapted && !adapt)),
+      "eps must be finite and > 0 (or 0 after hmc_adapt: the adapted per-chain steps)");
+  CFG(!adapt || (delta > 0 && delta < 1), "delta must lie in (0, 1)");
   CFG(L >= 0, "L must be >= 0");
   CFG(S >= 1, "S must be >= 1");
   CFG(iter0 >= 0 && iter0 + S <= (int64_t)1 << 32, "iter must lie in [0, 2^32)");
@@ -1134,8 +1142,20 @@ static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, doubl
   cpy(ctx->cur_theta, theta, Ck * 4, ctx->st, err);
   cpy(ctx->cur_grad, grad, Ck * 4, ctx->st, err);
   cpy(ctx->cur_logp, logp, ctx->C * 8, ctx->st, err);
-  set_rec(ctx, d_samples, d_acc, d_dH, S, iter0, eps, err);
+  if (adapt) {
+    k_da_init<<<1, 256, 0, ctx->st>>>(ctx->d_eps, ctx->d_da, ctx->C, eps);
+    set_rec(ctx, d_samples, d_acc, d_dH, S, iter0, 0.0, err, 1, delta);
+  } else {
+    set_rec(ctx, d_samples, d_acc, d_dH, S, iter0, eps, err);
+  }
   for (int s = 0; s < S; ++s) CK(cudaGraphLaunch(ctx->traj_exec, ctx->st));
+  if (adapt) {
+    double* d_out = (double*)tmp_alloc((size_t)ctx->C * 8);
+    k_da_finish<<<1, 256, 0, ctx->st>>>(ctx->d_eps, ctx->d_da, ctx->C, d_out);
+    CK(cudaMemcpyAsync(eps_bar, d_out, (size_t)ctx->C * 8, cudaMemcpyDefault, ctx->st));
+    host = true;
+    ctx->adapted = true;
+  }
   cpy(theta, ctx->cur_theta, Ck * 4, ctx->st, err);
   cpy(grad, ctx->cur_grad, Ck * 4, ctx->st, err);
   cpy(logp, ctx->cur_logp, ctx->C * 8, ctx->st, err);
@@ -1154,6 +1174,14 @@ int hmc_trajectory(hmc_ctx* ctx, float* theta, double* logp, float* grad, double
 int hmc_sample(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
                int32_t S, float* samples, uint8_t* acc, double* dH, void* stream) {
   return run_traj(ctx, theta, logp, grad, eps, L, iter0, S, samples, acc, dH, stream);
+}
+int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0, int32_t L, int64_t iter0,
+              int32_t n_adapt, double delta, double* eps_bar, uint8_t* acc, double* dH, void* stream) {
+  if (!eps_bar) {
+    g_err = "config: eps_bar must be non-NULL";
+    return HMC_E_CONFIG;
+  }
+  return run_traj(ctx, theta, logp, grad, eps0, L, iter0, n_adapt, nullptr, acc, dH, stream, 1, delta, eps_bar);
 }
 
 int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,

@@ -14,6 +14,8 @@ struct Rec {
   int64_t S;
   int64_t sidx;     // current sample slot
   int64_t iter;     // Philox iteration counter
+  int32_t adapt;    // 1: dual-averaging step-size adaptation after every trajectory (NEXT-2)
+  double delta;     // its target acceptance statistic
 };
 
 // Everything the per-chain state kernels need.
@@ -35,7 +37,8 @@ struct KState {
   const double* lik;           // [C] sum of squared residuals
   double inv_2s2;              // 1 / (2 sigma^2)
   double inv_sp2;              // 1 / sigma_p^2
-  const double* eps;           // device scalar step size
+  double* eps;                 // [C] per-chain step sizes (device)
+  double* da;                  // [C x 4] dual-averaging state: mu, Hbar, log epsbar, m
   Rec* rec;
   uint32_t key0, key1;
 };
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(KT) k_reduce_partials(const double* __restrict
 __global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
   __shared__ double red[KT / 32];
   const int c = blockIdx.x;
-  const double eps = (mode != 0) ? *s.eps : 0.0;
+  const double eps = (mode != 0) ? s.eps[c] : 0.0;
   const float fe = (float)eps, fh = (float)(0.5 * eps);
   double ss = 0.0;
   for (int64_t j = threadIdx.x; j < s.k; j += KT) {
@@ -370,11 +373,11 @@ __global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
 //      full kick p += eps g, drift theta += eps M^-1 p, scatter.  log pi is not needed at the
 //      inner points (only at the trajectory end, k_finalize mode 2), so no reduction here ----
 __global__ void __launch_bounds__(256) k_leapfrog(KState s) {
-  const float fe = (float)(*s.eps);
   const int64_t total = (int64_t)s.C * s.k;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = t / s.k, j = t - c * s.k;
+    const float fe = (float)s.eps[c];
     float th = s.wrk_theta[t];
     const float g = s.gl[t] - (float)((double)th * s.inv_sp2);
     s.wrk_grad[t] = g;
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(KT) k_traj_begin(KState s, int L0) {
   const int c = blockIdx.x;
   const uint32_t iter = (uint32_t)s.rec->iter;
   const uint32_t chain = s.chain_ids[c];
-  const double eps = *s.eps;
+  const double eps = s.eps[c];
   const float fe = (float)eps, fh = (float)(0.5 * eps);
   double K0 = 0.0;
   const int64_t nb = (s.k + 3) / 4;
@@ -457,6 +460,21 @@ __global__ void __launch_bounds__(KT) k_mh(KState s) {
     if (acc) s.cur_logp[c] = s.wrk_logp[c];
     if (rec->acc) rec->acc[(int64_t)c * rec->S + sidx] = (uint8_t)acc;
     if (rec->dH) rec->dH[(int64_t)c * rec->S + sidx] = H1 - H0;
+    if (rec->adapt) {
+      // dual averaging (Hoffman & Gelman Algorithm 5; DESIGN.md NEXT-2): gamma 0.05,
+      // t0 10, kappa 0.75; alpha = min(1, exp(H0 - H*)), 0 for a non-finite H*
+      double* da = s.da + (int64_t)c * 4;
+      const double alpha = isfinite(H1) ? ((H0 - H1 >= 0.0) ? 1.0 : exp(H0 - H1)) : 0.0;
+      const double m = da[3] + 1.0;
+      const double eta = 1.0 / (m + 10.0);
+      const double hbar = (1.0 - eta) * da[1] + eta * (rec->delta - alpha);
+      const double log_eps = da[0] - sqrt(m) / 0.05 * hbar;
+      const double w = pow(m, -0.75);
+      da[1] = hbar;
+      da[2] = w * log_eps + (1.0 - w) * da[2];
+      da[3] = m;
+      s.eps[c] = exp(log_eps);  // the next trajectory's step
+    }
   }
   __syncthreads();
   const int acc = acc_s;
@@ -472,6 +490,27 @@ __global__ void __launch_bounds__(KT) k_mh(KState s) {
     }
     if (rec->samples) rec->samples[((int64_t)c * rec->S + sidx) * s.k + j] = th;
   }
+}
+
+// dual-averaging start (mu = log(10 eps0), Hbar = 0, log epsbar = 0, m = 0; eps = eps0) and
+// finish (eps = epsbar, copied out)
+__global__ void k_da_init(double* __restrict__ eps, double* __restrict__ da, int C, double eps0) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    eps[c] = eps0;
+    da[4 * c + 0] = log(10.0 * eps0);
+    da[4 * c + 1] = 0.0;
+    da[4 * c + 2] = 0.0;
+    da[4 * c + 3] = 0.0;
+  }
+}
+__global__ void k_da_finish(double* __restrict__ eps, const double* __restrict__ da, int C, double* __restrict__ out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+    eps[c] = exp(da[4 * c + 2]);
+    out[c] = eps[c];
+  }
+}
+__global__ void k_fill_d(double* __restrict__ p, int n, double v) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) p[c] = v;
 }
 
 __global__ void k_advance(Rec* rec) {
