@@ -912,9 +912,10 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
   if (x->Ptc > 0) {
     x->Whi = dalloc<float>(x, (size_t)C * x->Ptc, err);
-    // default: one raw fp32 plane, split in shared memory by the GEMM converters (half the L2
-    // traffic of pre-split hi/lo planes; the engine is bound by L2 -> SM bandwidth)
-    if (getenv("HMC_TC_PRESPLIT")) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    // default: tf32 hi / lo planes written by the scatter (no B conversion in the GEMM);
+    // HMC_TC_RAWB=1: one raw plane split in shared memory by the converters (half the L2
+    // traffic, measured 2-3 % slower: the converters are on the critical path)
+    if (!getenv("HMC_TC_RAWB")) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
     x->d_tcpos = dalloc<int64_t>(x, x->k, err);
     CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 8, cudaMemcpyHostToDevice));
     for (auto& L : x->layers)
