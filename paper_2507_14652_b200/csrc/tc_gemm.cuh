@@ -44,10 +44,14 @@ constexpr int BM = 128;    // UMMA M (cta_group::1)
 constexpr int BK = 32;     // fp32 elements per K block (one 128-byte swizzle row)
 constexpr int NCONV = 4;   // converter warps: one per TMEM lane quadrant (A rows -> TMEM)
 constexpr int NEPI = 8;    // epilogue warps
-constexpr int NT = (3 + NCONV + NEPI) * 32;  // 480 threads
+constexpr int NT = (4 + NCONV + NEPI) * 32;  // 512 threads
 // Warp roles.  The warp schedulers favour higher warp ids, so the latency-critical single-lane
-// roles get the highest ids: epilogue 0-7, converters 8-11, A producer 12, B producer 13, MMA 14.
-constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TMA_A + 1, W_MMA = W_TMA_B + 1;
+// roles get the highest ids: epilogue 0-7, converters 8-11, A producer 12, B producer 13, MMA
+// issuers 14 (even K blocks) and 15 (odd K blocks): while one issuer is blocked feeding the
+// tensor pipe its K block, the other has already passed the barriers of the next one, so the
+// pipe does not drain between K blocks.
+constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TMA_A + 1, W_MMA = W_TMA_B + 1,
+              W_MMA2 = W_MMA + 1;
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
 template <int BN>
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-  } else if (warp == W_MMA) {
+  } else if (warp == W_MMA || warp == W_MMA2) {
     // ================================ MMA issuer ==================================
     // per K block, into the block's own accumulator (folded by the epilogue): the 8 small
     // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
@@ -500,11 +504,13 @@ __global__ void __launch_bounds__(NT, 1)
       // by adding byte offsets >> 4 (all shared addresses < 256 KB)
       const uint64_t dB0 = sdesc(su32(sBr), b_lbo, b_sbo, b_lay);
       const uint32_t kstep16 = (B_MN ? mn.kstep : 32) >> 4;
-      int s = 0;
-      uint32_t ph = 0;
-      uint32_t jb = 0;  // K blocks issued so far
+      const uint32_t mine = (warp == W_MMA2) ? 1u : 0u;  // K-block parity this issuer owns
+      uint32_t jb = 0;  // K blocks of this CTA so far (both issuers count all of them)
       for (int t = cid; t < total; t += ncl) {
         for (int kb = 0; kb < nk; ++kb, ++jb) {
+          if ((jb & 1u) != mine) continue;
+          const int s = (int)(jb % SB);
+          const uint32_t ph = (jb / SB) & 1u;
           const uint32_t buf = jb % NACC;
           const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
@@ -537,7 +543,6 @@ __global__ void __launch_bounds__(NT, 1)
           __syncwarp();
           if (mn.prof) pacc[2] += clock64() - t_i0;
           if (tl) g_tctl[3][jb] = clock64();
-          if (++s == SB) { s = 0; ph ^= 1; }
         }
       }
     }
