@@ -132,6 +132,15 @@ int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* 
 int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0, int32_t L, int64_t iter0,
               int32_t n_adapt, double delta, double* eps_bar, uint8_t* acc, double* dH, void* stream);
 
+/* Posterior predictive over the context's inputs (PAPER.md P:401 / P:480:
+ * predictions "mean ± 3 standard deviations" over the HMC samples): for S samples of theta_s
+ * (samples [S x k] fp32, host or device; the frozen entries stay at mu), mean[j] and var[j]
+ * (population variance) of F(x_j) over the samples, fp64, for every datum j (MLP: the n rows;
+ * DeepONet: the n_c x n_x pairs, row-major).  Predictions at new inputs: set up a context on
+ * those inputs.  Runs the forward pass C samples at a time; synchronous.  HMC_E_CONFIG on NULL
+ * arguments, S < 1 or a DATA-mode context. */
+int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, double* var, void* stream);
+
 /* Parameter sensitivities, the step before the hot path (Algorithm 2 "Compute: S_i^2",
  * PAPER.md eqn:sensitivities P:193-197):  S_i^2 = sigma_i^2 / N_d * sum_j (dF_mu(x_j)/dtheta_i)^2
  * for every flat parameter i (P = length of mu), gradients of the network OUTPUT at the VI mean

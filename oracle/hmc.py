@@ -189,3 +189,17 @@ def adapt_chain(target, theta0, eps0, L, iter0, n_adapt, delta, chain):
         accs.append(r["accepted"])
         alphas.append(a)
     return math.exp(st["log_epsbar"]), np.array(eps_used), np.array(accs), np.array(alphas), (theta, lp, g)
+
+
+# ---- posterior predictive ----
+def predictive(target, samples):
+    """Mean and (population) variance over the samples of F(x_j) for every datum j
+    (P:401 / P:480: predictions reported as mean +- 3 sd over the HMC samples).  The frozen
+    parameters stay at mu; MLP -> [n], DeepONet -> [n_c * n_x] row-major."""
+    vals = []
+    for th in np.asarray(samples, dtype=np.float64):
+        F = network.predict(target.arch, target.assemble(th), target.data)
+        vals.append(np.asarray(F, dtype=np.float64).ravel())
+    V = np.array(vals)
+    m = V.mean(axis=0)
+    return m, (V * V).mean(axis=0) - m * m

@@ -54,7 +54,7 @@ class hmc_config(ctypes.Structure):
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
-           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt"]
+           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -271,6 +271,21 @@ def hmc_adapt(ctx, theta, logp, grad, eps0, L, iter0, n_adapt, delta, acc=None, 
     return out
 
 
+def hmc_predict(ctx, samples, stream=None):
+    """Posterior predictive mean / variance over the inputs of `ctx` (a Context); samples [S x k]."""
+    keep = []
+    L = lib()
+    L.hmc_predict.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_void_p]
+    S = int(samples.shape[0])
+    N = int(getattr(ctx, "_n_out", 0))
+    mean = np.empty(N, dtype=np.float64)
+    var = np.empty(N, dtype=np.float64)
+    _check(L.hmc_predict(ctx.ctx, _ptr(samples, keep, np.float32), S, mean.ctypes.data, var.ctypes.data,
+                         _stream(stream)), ctx.ctx)
+    return mean, var
+
+
 def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):
     """S_i^2 for every flat parameter (eqn:sensitivities) of problem.arch on problem's data, at
     mu (default problem.frozen) with VI sds sigma_vi (default problem.sigma_vi).  Returns a
@@ -348,6 +363,7 @@ class Context:
             c.nccl_id = ctypes.addressof(idbuf)
         self.ctx = hmc_setup(a, d, c)
         self.C, self.k, self.P = C, c.k, c.P
+        self._n_out = int(d.n) if arch.kind == "mlp" else int(d.n_c * d.n_x)
 
     def close(self):
         if self.ctx:

@@ -1185,6 +1185,78 @@ int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0
   return run_traj(ctx, theta, logp, grad, eps0, L, iter0, n_adapt, nullptr, acc, dH, stream, 1, delta, eps_bar);
 }
 
+int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, double* var, void* stream) {
+  API_BEGIN(ctx)
+  CFG(samples && mean && var && S >= 1, "samples, mean, var must be non-NULL and S >= 1");
+  CFG(ctx->mode != HMC_MODE_DATA || ctx->world == 1, "hmc_predict runs on one rank's data (not DATA mode)");
+  cudaStream_t us = (cudaStream_t)stream;
+  hmc_ctx* x = ctx;
+  sync_in(x, us, err);
+  const int64_t N = x->kind == HMC_MLP ? x->n : x->n_c * x->n_x;
+  const int C = x->C;
+  DevBuf tmp;
+  auto tmp_alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    tmp.ptrs.push_back(p);
+    return p;
+  };
+  const float* dsamp = samples;
+  if (!is_device_ptr(samples)) {
+    float* d = (float*)tmp_alloc((size_t)S * x->k * 4);
+    CK(cudaMemcpyAsync(d, samples, (size_t)S * x->k * 4, cudaMemcpyHostToDevice, x->st));
+    dsamp = d;
+  }
+  double* dsum = (double*)tmp_alloc((size_t)N * 8);
+  double* dsq = (double*)tmp_alloc((size_t)N * 8);
+  double* dmean = (double*)tmp_alloc((size_t)N * 8);
+  double* dvar = (double*)tmp_alloc((size_t)N * 8);
+  CK(cudaMemsetAsync(dsum, 0, (size_t)N * 8, x->st));
+  CK(cudaMemsetAsync(dsq, 0, (size_t)N * 8, x->st));
+  const size_t Ck = (size_t)C * x->k;
+  for (int64_t s0 = 0; s0 < S; s0 += C) {
+    const int nb = (int)std::min<int64_t>(C, S - s0);
+    // batch of samples -> the chains' parameters (missing chains repeat the last sample)
+    for (int c = 0; c < C; ++c) {
+      const int64_t src = s0 + std::min(c, nb - 1);
+      CK(cudaMemcpyAsync(x->wrk_theta + (size_t)c * x->k, dsamp + src * x->k, x->k * 4, cudaMemcpyDeviceToDevice,
+                         x->st));
+    }
+    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
+    (void)Ck;
+    if (x->kind == HMC_MLP) {
+      NetInfo& Nn = x->nets[0];
+      const int nl = (int)Nn.layers.size();
+      for (int i = 0; i < nl - 1; ++i) enqueue_forward_hidden(x, Nn, i, x->st);
+      LayerInfo& O = x->layers[Nn.layers[nl - 1]];
+      int64_t s_in;
+      const float* in = layer_input(x, Nn, nl - 1, &s_in);
+      k_out_fwd<<<dim3(x->n_part, C), 256, O.n_in * sizeof(float), x->st>>>(
+          in, s_in, O.n_in, O.rows, x->Wd, x->P, O.w_off, O.b_off, nullptr, x->R, 0.0, x->part_sq, x->n_part);
+    } else {
+      for (int ni = 0; ni < 2; ++ni)
+        for (int i = 0; i < (int)x->nets[ni].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[ni], i, x->st);
+      const LayerInfo& Bl = x->layers[x->nets[0].layers.back()];
+      const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
+      const int p = Bl.n_out;
+      GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+      a.A = Bl.A; a.lda = p; a.sA = x->n_c * p;
+      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+      a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+      a.epi = EPI_STORE;
+      launch_gemm(x, a, true, true, x->st, "predict");
+    }
+    k_pred_accum<<<148 * 4, 256, 0, x->st>>>(x->R, N, nb, x->Wd, x->P, x->has_b0 ? x->b0_off : -1, dsum, dsq);
+    CK(cudaGetLastError());
+  }
+  k_pred_final<<<148 * 4, 256, 0, x->st>>>(dsum, dsq, N, (double)S, dmean, dvar);
+  CK(cudaMemcpyAsync(mean, dmean, (size_t)N * 8, cudaMemcpyDefault, x->st));
+  CK(cudaMemcpyAsync(var, dvar, (size_t)N * 8, cudaMemcpyDefault, x->st));
+  CK(cudaStreamSynchronize(x->st));  // temporaries are freed on return
+  sync_out(x, us, true, err);
+  API_END
+}
+
 int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
                     double* s2, void* stream) {
   if (!arch || !data || !mu || !sigma_vi || !s2) {

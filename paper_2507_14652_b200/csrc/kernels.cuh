@@ -116,9 +116,13 @@ __global__ void __launch_bounds__(256) k_out_fwd(const float* __restrict__ Ain, 
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
       const float f = s + bias;
-      const float r = y[n] - f;
-      R[(int64_t)c * rows + n] = (float)((double)r * inv_s2);
-      psq += (double)r * (double)r;
+      if (y) {
+        const float r = y[n] - f;
+        R[(int64_t)c * rows + n] = (float)((double)r * inv_s2);
+        psq += (double)r * (double)r;
+      } else {
+        R[(int64_t)c * rows + n] = f;  // prediction mode (hmc_predict): the output itself
+      }
     }
   }
   const double tot = block_sum_d<256>(psq, red);
@@ -266,6 +270,30 @@ __global__ void k_wgrad_narrow_p2(const float* __restrict__ part, int n_chunks, 
     float acc = 0.f;
     for (int ch = 0; ch < n_chunks; ++ch) acc += part[((int64_t)c * n_chunks + ch) * per + t];
     gl[(int64_t)c * k + sl] = acc;
+  }
+}
+
+// ---- posterior predictive (NEXT-4): per datum j, sum and sum of squares over samples of
+//      F_j = out[c][j] (+ b0 of sample c), chains in fixed order, fp64 ----
+__global__ void k_pred_accum(const float* __restrict__ out, int64_t N, int nb, const float* __restrict__ Wd, int64_t P,
+                             int64_t b0_off, double* __restrict__ sum, double* __restrict__ sumsq) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    double s = sum[j], q = sumsq[j];
+    for (int c = 0; c < nb; ++c) {
+      const double v = (double)out[(int64_t)c * N + j] + (b0_off >= 0 ? (double)Wd[(int64_t)c * P + b0_off] : 0.0);
+      s += v;
+      q += v * v;
+    }
+    sum[j] = s;
+    sumsq[j] = q;
+  }
+}
+__global__ void k_pred_final(const double* __restrict__ sum, const double* __restrict__ sumsq, int64_t N, double S,
+                             double* __restrict__ mean, double* __restrict__ var) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    const double m = sum[j] / S;
+    mean[j] = m;
+    var[j] = fmax(sumsq[j] / S - m * m, 0.0);
   }
 }
 
