@@ -141,6 +141,13 @@ int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0
  * arguments, S < 1 or a DATA-mode context. */
 int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, double* var, void* stream);
 
+/* Convergence diagnostics: split-R^ and effective sample
+ * size per parameter (Gelman et al., BDA3 eqs. 11.3-11.8, on split chains: m = 2C half-chains of
+ * n = S/2 draws; ESS truncated at the first odd lag T with rho_{T+1} + rho_{T+2} < 0).
+ * samples [C x S x k] fp32 (host or device; the layout hmc_sample writes), rhat / ess [k] fp64
+ * out (host or device).  Synchronous.  HMC_E_CONFIG unless 1 <= C <= 1024, S >= 4, k >= 1. */
+int hmc_diagnostics(const float* samples, int32_t C, int64_t S, int64_t k, double* rhat, double* ess, void* stream);
+
 /* Parameter sensitivities, the step before the hot path (Algorithm 2 "Compute: S_i^2",
  * PAPER.md eqn:sensitivities P:193-197):  S_i^2 = sigma_i^2 / N_d * sum_j (dF_mu(x_j)/dtheta_i)^2
  * for every flat parameter i (P = length of mu), gradients of the network OUTPUT at the VI mean

@@ -14,9 +14,12 @@ Plain, slow, obviously-correct NumPy float64 implementation of:
                 draw, kick-drift-kick leapfrog, Metropolis-Hastings step, chains
   sensitivity.py - parameter sensitivities S_i^2 (eqn:sensitivities) and the tau-partition
                 (eqn:threshold) of the step before the hot path
+  diagnostics.py - split-R^ and effective sample size (BDA3 §11.4-11.5; NEXT-4)
+  (hmc.py also holds the dual-averaging step-size adaptation (NEXT-2) and the posterior
+  predictive (NEXT-4))
 
 Each function cites the PAPER.md passage (P:line) or SURVEY.md reading it follows.
 Parity status: every function is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
 (closed forms, finite differences, invariants, known answers); see DESIGN.md §4.
 """
-from . import network, philox, hmc, sensitivity  # noqa: F401
+from . import network, philox, hmc, sensitivity, diagnostics  # noqa: F401

@@ -54,7 +54,8 @@ class hmc_config(ctypes.Structure):
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
-           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict"]
+           "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict",
+           "hmc_diagnostics"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -284,6 +285,20 @@ def hmc_predict(ctx, samples, stream=None):
     _check(L.hmc_predict(ctx.ctx, _ptr(samples, keep, np.float32), S, mean.ctypes.data, var.ctypes.data,
                          _stream(stream)), ctx.ctx)
     return mean, var
+
+
+def hmc_diagnostics(samples, stream=None):
+    """split-R^ and ESS per parameter of samples [C x S x k] (include/hmc.h hmc_diagnostics)."""
+    keep = []
+    L = lib()
+    L.hmc_diagnostics.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    C, S, k = (int(v) for v in samples.shape)
+    rhat = np.empty(k, dtype=np.float64)
+    ess = np.empty(k, dtype=np.float64)
+    _check(L.hmc_diagnostics(_ptr(samples, keep, np.float32), C, S, k, rhat.ctypes.data, ess.ctypes.data,
+                             _stream(stream)))
+    return rhat, ess
 
 
 def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):

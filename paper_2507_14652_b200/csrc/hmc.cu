@@ -1257,6 +1257,38 @@ int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, dou
   API_END
 }
 
+int hmc_diagnostics(const float* samples, int32_t C, int64_t S, int64_t k, double* rhat, double* ess, void* stream) {
+  if (!samples || !rhat || !ess || C < 1 || C > 1024 || S < 4 || k < 1) {
+    g_err = "config: samples, rhat, ess non-NULL; 1 <= C <= 1024, S >= 4, k >= 1";
+    return HMC_E_CONFIG;
+  }
+  std::string err;
+  hmc_ctx dummy;
+  hmc_ctx* x = &dummy;
+  try {
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t tot = (size_t)C * S * k;
+    const float* d = samples;
+    if (!is_device_ptr(samples)) {
+      float* t = dalloc<float>(x, tot, err);
+      CK(cudaMemcpyAsync(t, samples, tot * 4, cudaMemcpyHostToDevice, st));
+      d = t;
+    }
+    double* dr = dalloc<double>(x, (size_t)k, err);
+    double* de = dalloc<double>(x, (size_t)k, err);
+    const int grid = (int)std::min<int64_t>(k, 148 * 8);
+    k_diag<<<grid, DIAG_T, 0, st>>>(d, C, S, k, dr, de);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(rhat, dr, (size_t)k * 8, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(ess, de, (size_t)k * 8, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+  } catch (Fail f) {
+    g_err = err;
+    return f.code;
+  }
+  return HMC_OK;
+}
+
 int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
                     double* s2, void* stream) {
   if (!arch || !data || !mu || !sigma_vi || !s2) {

@@ -297,6 +297,89 @@ __global__ void k_pred_final(const double* __restrict__ sum, const double* __res
   }
 }
 
+// ---- convergence diagnostics (NEXT-4, BDA3 §11.4-11.5 on split chains): one block per
+//      parameter j; samples[c][s][j]; half-chain h < C is chain h's first n draws, h >= C the
+//      last n draws of chain h - C (n = S / 2, m = 2C).  fp64, fixed-order reductions ----
+constexpr int DIAG_T = 256;
+__device__ __forceinline__ double diag_val(const float* x, int h, int C, int64_t S, int64_t k, int64_t n, int64_t i,
+                                           int64_t j) {
+  const int c = h < C ? h : h - C;
+  const int64_t off = h < C ? 0 : S - n;
+  return (double)x[((int64_t)c * S + off + i) * k + j];
+}
+__global__ void __launch_bounds__(DIAG_T) k_diag(const float* __restrict__ x, int C, int64_t S, int64_t k,
+                                                 double* __restrict__ rhat, double* __restrict__ ess) {
+  __shared__ double hm[2 * 1024], hv[2 * 1024];  // per half-chain mean / variance (m <= 2048)
+  __shared__ double red[DIAG_T / 32];
+  __shared__ double sh[4];
+  const int m = 2 * C;
+  const int64_t n = S / 2;
+  for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+    for (int h = threadIdx.x; h < m; h += DIAG_T) {
+      double su = 0.0;
+      for (int64_t i = 0; i < n; ++i) su += diag_val(x, h, C, S, k, n, i, j);
+      const double mu = su / (double)n;
+      double q = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        const double d = diag_val(x, h, C, S, k, n, i, j) - mu;
+        q += d * d;
+      }
+      hm[h] = mu;
+      hv[h] = q / (double)(n - 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double W = 0.0, mm = 0.0;
+      for (int h = 0; h < m; ++h) { W += hv[h]; mm += hm[h]; }
+      W /= m;
+      mm /= m;
+      double B = 0.0;
+      for (int h = 0; h < m; ++h) B += (hm[h] - mm) * (hm[h] - mm);
+      B /= (m - 1);
+      const double vp = (double)(n - 1) / (double)n * W + B;
+      sh[0] = W;
+      sh[1] = vp;
+      rhat[j] = sqrt(vp / W);
+    }
+    __syncthreads();
+    const double vp = sh[1];
+    // rho_t on demand (block reduction of the variogram)
+    auto rho = [&](int64_t t) -> double {
+      double v = 0.0;
+      const int64_t per = n - t, tot = (int64_t)m * per;
+      for (int64_t q = threadIdx.x; q < tot; q += DIAG_T) {
+        const int h = (int)(q / per);
+        const int64_t i = t + (q - (int64_t)h * per);
+        const double d = diag_val(x, h, C, S, k, n, i, j) - diag_val(x, h, C, S, k, n, i - t, j);
+        v += d * d;
+      }
+      v = block_sum_d<DIAG_T>(v, red);
+      if (threadIdx.x == 0) sh[2] = 1.0 - (v / ((double)m * (double)per)) / (2.0 * vp);
+      __syncthreads();
+      const double r = sh[2];
+      __syncthreads();
+      return r;
+    };
+    double ssum = 0.0;
+    double r1 = n > 1 ? rho(1) : 0.0, r2 = n > 2 ? rho(2) : 0.0;
+    for (int64_t t = 1; t < n; ++t) {
+      // invariant: r1 = rho_t, r2 = rho_{t+1} (when t + 1 < n)
+      ssum += r1;
+      if (t + 2 < n) {
+        const double r3 = rho(t + 2);
+        if (r2 + r3 < 0.0) break;
+        r1 = r2;
+        r2 = r3;
+      } else {
+        r1 = r2;
+        r2 = 0.0;
+      }
+    }
+    if (threadIdx.x == 0) ess[j] = (double)m * (double)n / (1.0 + 2.0 * ssum);
+    __syncthreads();
+  }
+}
+
 // ---- sensitivity step (NEXT-1, eqn:sensitivities P:193-197) ----
 __global__ void k_fill(float* __restrict__ p, int64_t n, float v) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
