@@ -320,7 +320,8 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
 struct MnDesc {
   uint32_t lbo = 4096, sbo = 512, layout = 1, kstep = 1024;
   int pf = 0;    // L2 prefetch distance of the TMA producer, in K blocks (0 = off)
-  int prof = 0;  // accumulate per-role wait cycles into g_tcprof[vid]
+  int prof = 0;  // 1: accumulate per-role wait cycles into g_tcprof[vid]; 2 + v: also record the
+                 //    CTA-0 timeline of launches of kernel variant v
   int vid = 0;   // kernel variant (index in tc_variants)
   int dbg = 0;   // dev experiments: 1 = no MMAs, 2 = no converter work, 4 = no epilogue fold (results wrong)
 };
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(NT, 1)
         tile_of(t, b, mt, nt);
         for (int kb = 0; kb < nk; ++kb, ++jq) {
           mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0]);
-          if (mn.prof == 2 && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
+          if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
           // both CTAs of the pair receive the whole B stage: pre-split -> rank r loads plane r;
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(NT, 1)
           const int s = (int)(jb % SB);
           const uint32_t ph = (jb / SB) & 1u;
           const uint32_t buf = jb % NACC;
-          const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+          const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
           mbar_wait_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
           if (tl) g_tctl[1][jb] = clock64();
@@ -559,7 +560,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         // A first (the TMEM slot write is the long pole), then raw B planes if any
         mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0]);
-        const bool tlc = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+        const bool tlc = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
         if (tlc) atomicMax(&g_tctl[6][jb], clock64());  // last converter warp has A
         const uint8_t* stA = sAr + sa * C_::A_BYTES;
         uint32_t hi[32], lo[32];
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
           uint8_t* stB = sBr + sb * C_::B_STAGE;
           mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
-          if (mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0) atomicMax(&g_tctl[4][jb], clock64());
+          if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0) atomicMax(&g_tctl[4][jb], clock64());
           float4* bh = (float4*)stB;
           float4* bl = (float4*)(stB + C_::B_BYTES);
 #pragma unroll 4
@@ -726,8 +727,8 @@ __global__ void __launch_bounds__(NT, 1)
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NACC;
         mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0]);
-        const bool tl = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
-        const bool tla = mn.prof == 2 && blockIdx.x == 0 && jb < TL_N && lane == 0;
+        const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
+        const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;

@@ -1,7 +1,7 @@
 """Dev diagnostic: CTA-0 pipeline timeline of one tcgen05 GEMM (HMC_TC_PROF=2) via the debug GEMM:
 C = A B with M=2048, N=256, K=256 (the cfg5 trunk forward shape), 64 chains."""
 import os, sys
-os.environ["HMC_TC_PROF"] = "2"
+os.environ.setdefault("HMC_TC_PROF", "2")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2507_14652_b200 import abi
