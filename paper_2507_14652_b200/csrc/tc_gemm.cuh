@@ -649,20 +649,29 @@ __global__ void __launch_bounds__(NT, 1)
     float4* srow_base = reinterpret_cast<float4*>(stg0 + lane * 128);  // row `lane`, chunk q at q ^ (lane & 7)
     // parked tile: pend groups left (emitted in order), its batch / row block / first column
     int pend = 0, p_next = 0, p_b = 0, p_m0 = 0, p_nb = 0, p_blk = 0, p_ng = 0;
-    auto emit_group = [&](int g) {
+    // the parked tile is emitted in steps, one per fold of the next tile: EPI_FWD with tanh takes
+    // 3 steps per 32-column group (12 / 12 / 8 columns of tanh, then the store), others 1 step;
+    // with 8 K blocks per tile the last store is issued two folds before the tile end, so its
+    // read of the staging tile has completed when the next tile is parked
+    const int nstep = (EPI == EPI_FWD && a.act == ACT_TANH) ? 3 : 1;
+    auto emit_step = [&](int k) {
       if (mn.dbg & 8) return;  // dev experiment: no output traffic
+      const int g = k / nstep, part = k - g * nstep;
       uint8_t* stg = stg0 + g * STG;
       float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
       const int n0 = p_nb + 32 * g;
       if (EPI == EPI_FWD && a.act == ACT_TANH) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int qq = 0; qq < 3; ++qq) {
+          const int q = 3 * part + qq;
+          if (q >= 8) break;
           float4 z = srow[q ^ (lane & 7)];
           tanh_acc2(z.x, z.y);
           tanh_acc2(z.z, z.w);
           srow[q ^ (lane & 7)] = z;
         }
       }
+      if (part != nstep - 1) return;
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
@@ -716,13 +725,20 @@ __global__ void __launch_bounds__(NT, 1)
         prefetched = true;
       }
       // ---- fold the K-block partials into round-to-nearest fp32 sums ----
-      // (EPI_FWD: the sums start from the bias, loaded while the first K block is in flight)
+      // (EPI_FWD: the warp's NC bias values are loaded now, NC/32 per lane, and only consumed at
+      // the tile end - the load latency hides behind the folds instead of stalling the first)
       float acc[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) acc[i] = 0.f;
+      float bias_l[NC / 32];
       {
         const int nb = nt * BN + half * NC;
         const float* bias = (EPI == EPI_FWD && a.bias) ? a.bias + (int64_t)b * a.s_bias + nb : nullptr;
 #pragma unroll
-        for (int i = 0; i < NC; ++i) acc[i] = (bias && nb + i < a.N) ? __ldg(bias + i) : 0.f;
+        for (int u = 0; u < NC / 32; ++u) {
+          const int col = u * 32 + lane;
+          bias_l[u] = (bias && nb + col < a.N) ? __ldg(bias + col) : 0.f;
+        }
       }
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NACC;
@@ -748,9 +764,9 @@ __global__ void __launch_bounds__(NT, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
-        if (pend > 0) {  // one group of the parked tile per K block
+        if (pend > 0) {  // one step of the parked tile per K block
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
-          emit_group(p_next++);
+          emit_step(p_next++);
           if (--pend == 0 && loadx && !prefetched) {
             staging_free();
             issue_prefetch(b, mt, nt);
@@ -761,7 +777,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       const unsigned long long t_out0 = mn.prof ? clock64() : 0ull;
       while (pend > 0) {  // short K: flush the parked tile
-        emit_group(p_next++);
+        emit_step(p_next++);
         --pend;
       }
       if (loadx && !prefetched) {
@@ -769,6 +785,10 @@ __global__ void __launch_bounds__(NT, 1)
         issue_prefetch(b, mt, nt);
       }
       if (!loadx) staging_free();
+      if (EPI == EPI_FWD) {  // + bias (column u*32 + l lives in lane l's bias_l[u])
+#pragma unroll
+        for (int i = 0; i < NC; ++i) acc[i] += __shfl_sync(0xffffffffu, bias_l[i >> 5], i & 31);
+      }
       // ---- tile end: the register part of the fused epilogue, parked in staging ----
       if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
       const int m = mt * BM + 32 * quad + lane;
@@ -866,7 +886,7 @@ __global__ void __launch_bounds__(NT, 1)
         for (int q = 0; q < 8; ++q) srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
       if (EPI != EPI_WGRAD) {  // park the tile
-        pend = ng; p_next = 0; p_b = b; p_m0 = mt * BM + 32 * quad; p_nb = nt * BN + half * NC;
+        pend = ng * nstep; p_next = 0; p_b = b; p_m0 = mt * BM + 32 * quad; p_nb = nt * BN + half * NC;
         p_blk = mt * 4 + quad;
         __syncwarp();
       }
@@ -890,7 +910,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     while (pend > 0) {  // the last parked tile
-      emit_group(p_next++);
+      emit_step(p_next++);
       --pend;
     }
     if (lane == 0) bulk_wait0();
