@@ -54,10 +54,13 @@ constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TM
               W_MMA2 = W_MMA + 1;
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
 
-template <int BN>
+// WG: the weight-gradient layout - no output staging (the epilogue writes the compacted k-vector
+// from registers), the freed shared memory deepens the B ring, whose raw planes the epilogue
+// warps split (they are idle between folds there; the converters keep A only)
+template <int BN, bool WG = false>
 struct Cfg {
   static constexpr int SA = 4;                          // raw A ring (released by the converters)
-  static constexpr int SB = 3;                          // B ring (released by the MMA)
+  static constexpr int SB = WG ? 5 : 3;                 // B ring (released by the MMA)
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
   static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
   static constexpr int B_STAGE = 2 * B_BYTES;           // hi + lo planes
@@ -72,7 +75,9 @@ struct Cfg {
   static constexpr int NGRP = NC / 32;                  // 32-column groups per epilogue thread
   static constexpr int B_OFF = SA * A_BYTES;
   static constexpr int STG_OFF = B_OFF + SB * B_STAGE;
-  static constexpr int SMEM = 1024 /*align*/ + STG_OFF + NEPI * NGRP * STG + 512 /*barriers*/;
+  static constexpr int STG_BYTES = WG ? 0 : NEPI * NGRP * STG;
+  static constexpr int SMEM = 1024 /*align*/ + STG_OFF + STG_BYTES + 512 /*barriers*/;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
 // ---------------------------------------------------------------- PTX wrappers (sm_100a) ---
@@ -136,7 +141,7 @@ __device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
 // 2 full_op ok, 3 issued, 4 epilogue tfull ok, 5 epilogue folded, 6 converter full (A) ok,
 // 7 converter arrive full_op
 constexpr int TL_N = 256;
-__device__ unsigned long long g_tctl[8][TL_N];
+__device__ unsigned long long g_tctl[16][TL_N];
 __device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
   if (!on) { mbar_wait(b, parity); return; }
   const unsigned long long t0 = clock64();
@@ -360,8 +365,11 @@ __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                    const __grid_constant__ CUtensorMap mB2, const __grid_constant__ CUtensorMap mC,
                    const __grid_constant__ CUtensorMap mX, GemmArgs a, MnDesc mn) {
-  using C_ = Cfg<BN>;
+  using C_ = Cfg<BN, EPI == EPI_WGRAD>;
   constexpr int SA = C_::SA, SB = C_::SB, NACC = C_::NACC, NC = C_::NC, NGRP = C_::NGRP;
+  // raw B planes split by the epilogue warps (EPI_WGRAD), ESPLIT_D K blocks ahead of the fold
+  constexpr bool ESPLIT = (EPI == EPI_WGRAD) && !B_PRE;
+  constexpr uint32_t ESPLIT_D = 2;
   // EPI_DACT reads act'(dsrc) and EPI_RESID reads V tile by tile: TMA-loaded (mX) into the
   // staging buffers while the tile's K blocks are still in flight
   const bool loadx = (EPI == EPI_RESID) || (EPI == EPI_DACT && a.act != ACT_ID);
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sAr = smem;                  // raw A ring [SA][A_BYTES]
   uint8_t* sBr = smem + C_::B_OFF;      // B ring [SB][hi | lo]
   uint8_t* stg_base = smem + C_::STG_OFF;
-  uint64_t* bar = (uint64_t*)(stg_base + NEPI * NGRP * STG);
+  uint64_t* bar = (uint64_t*)(stg_base + C_::STG_BYTES);
   uint64_t* a_full = bar;                         // [SA]   TMA -> converters
   uint64_t* a_empty = a_full + SA;                // [SA]   converters (A read) -> A producer
   uint64_t* b_full = a_empty + SA;                // [SB]   TMA -> converters
@@ -384,8 +392,9 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* tfull = afree + C_::NAS;              // [NACC] MMA -> epilogue (K-block partial ready)
   uint64_t* tempty = tfull + NACC;                // [NACC] epilogue -> MMA (partial folded)
   uint64_t* xfull = tempty + NACC;                // [NEPI] per epilogue warp: mX tiles landed
-  uint32_t* tmem_holder = (uint32_t*)(xfull + NEPI);
-  double* red = (double*)(xfull + NEPI + 1);      // [2 x NEPI] epilogue reductions
+  uint64_t* bsplit = xfull + NEPI;                // [SB]   epilogue (raw B split) -> MMA (ESPLIT)
+  uint32_t* tmem_holder = (uint32_t*)(bsplit + SB);
+  double* red = (double*)(bsplit + SB + 1);       // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -424,6 +433,7 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&tempty[i], NEPI);  // one arrive per epilogue warp
     }
     for (int i = 0; i < NEPI; ++i) mbar_init(&xfull[i], 1);
+    for (int i = 0; i < SB; ++i) mbar_init(&bsplit[i], NEPI);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
     tma_prefetch(&mB);
@@ -519,7 +529,8 @@ __global__ void __launch_bounds__(NT, 1)
           if (tl) g_tctl[1][jb] = clock64();
           tc_fence_after();
           mbar_wait_t(&full_op[jb % C_::NAS], (jb / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
-          if (B_PRE) mbar_wait(&b_full[s], ph);  // (raw B planes are waited for by the converters)
+          if (B_PRE) mbar_wait(&b_full[s], ph);  // (raw B planes are waited for by their splitters)
+          if (ESPLIT) mbar_wait(&bsplit[s], ph);
           if (tl) g_tctl[2][jb] = clock64();
           tc_fence_after();
           const uint32_t dcol = tmem_base + buf * BN;
@@ -592,21 +603,26 @@ __global__ void __launch_bounds__(NT, 1)
             lo[k] = __float_as_uint(x - h);
           }
         }
+        const bool tc0 = tlc && warp == W_CONV0;  // converter warp 0 phase stamps
+        if (tc0) g_tctl[8][jb] = clock64();
         const uint32_t as = jb % C_::NAS;
         mbar_wait_t(&afree[as], ((jb / C_::NAS) & 1) ^ 1, mn.prof, pacc[1]);
         tc_fence_after();
+        if (tc0) g_tctl[9][jb] = clock64();
         if (!(mn.dbg & 2)) {
           tmem_st32(ta + as * 64, hi);
           tmem_st32(ta + as * 64 + 32, lo);
         }
-        if (!B_PRE) {  // B planes in shared memory: hi in place, lo beside it
+        if (tc0) g_tctl[10][jb] = clock64();
+        if (!B_PRE && !ESPLIT) {  // B planes in shared memory: hi in place, lo beside it
           uint8_t* stB = sBr + sb * C_::B_STAGE;
           mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
           if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0) atomicMax(&g_tctl[4][jb], clock64());
+          if (tc0) g_tctl[11][jb] = clock64();
           float4* bh = (float4*)stB;
           float4* bl = (float4*)(stB + C_::B_BYTES);
 #pragma unroll 4
-          for (int i = ct; i < C_::B_BYTES / 16; i += NCONV * 32) {
+          for (int i = ct; i < ((mn.dbg & 64) ? 0 : C_::B_BYTES / 16); i += NCONV * 32) {  // 64: dev experiment
             float4 x = bh[i];
             if (EPI == EPI_WGRAD && a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
             float4 h, l;
@@ -615,19 +631,23 @@ __global__ void __launch_bounds__(NT, 1)
             bh[i] = h;
             bl[i] = l;
           }
+          if (tc0) g_tctl[12][jb] = clock64();
         }
         // publish: A in TMEM (wait::st), B planes visible to the async proxy (the proxy fence
         // also orders this warp's raw-A reads before the A producer's next TMA write)
         // (one elected arrive per warp after __syncwarp: per-thread arrives serialise on the
         // SM's barrier unit and cost more than the whole K block of MMAs)
         tmem_wait_st();
+        if (tc0) g_tctl[13][jb] = clock64();
         fence_proxy_async();
         tc_fence_before();
+        if (tc0) g_tctl[14][jb] = clock64();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&full_op[as]);
           mbar_arrive(&a_empty[sa]);
         }
+        if (tc0) g_tctl[15][jb] = clock64();
         if (tlc) atomicMax(&g_tctl[7][jb], clock64());  // last converter warp published
         if (++sa == SA) { sa = 0; pha ^= 1; }
         if (++sb == SB) { sb = 0; phb ^= 1; }
@@ -713,6 +733,32 @@ __global__ void __launch_bounds__(NT, 1)
       }
       __syncwarp();
     };
+    // ESPLIT: raw B stages of this CTA's K blocks [js, lim) split in place (hi) and beside (lo),
+    // each warp one eighth of the stage
+    const uint32_t my_kb = (cid < total) ? (uint32_t)((total - cid + ncl - 1) / ncl) * (uint32_t)nk : 0u;
+    uint32_t js = 0;
+    auto split_upto = [&](uint32_t lim) {
+      for (; js < lim && js < my_kb; ++js) {
+        const int s = (int)(js % SB);
+        mbar_wait(&b_full[s], (js / SB) & 1u);
+        float4* bh = (float4*)(sBr + s * C_::B_STAGE);
+        float4* bl = (float4*)(sBr + s * C_::B_STAGE + C_::B_BYTES);
+#pragma unroll
+        for (int i = ew * 32 + lane; i < C_::B_BYTES / 16; i += NEPI * 32) {
+          float4 x = bh[i];
+          if (a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
+          float4 h, l;
+          h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          bh[i] = h;
+          bl[i] = l;
+        }
+        fence_proxy_async();  // generic-proxy writes -> the tensor core's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bsplit[s]);
+      }
+    };
+    if (ESPLIT) split_upto(ESPLIT_D);
     uint32_t jb = 0, jt = 0;
     for (int t = cid; t < total; t += ncl, ++jt) {
       int b, mt, nt;
@@ -764,6 +810,7 @@ __global__ void __launch_bounds__(NT, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
         if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
+        if (ESPLIT) split_upto(jb + 1 + ESPLIT_D);
         if (pend > 0) {  // one step of the parked tile per K block
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
           emit_step(p_next++);
@@ -960,10 +1007,12 @@ struct TcVariant {
   bool amn, bmn, pre;
   int epi;
   TcKernel fn;
+  int smem;  // dynamic shared memory bytes
 };
 template <int BN>
 inline const TcVariant* tc_variants(int* n) {
-#define TV(AMN, BMN, PRE, EPI) {AMN, BMN, PRE, EPI, (TcKernel)tc::tc_gemm_kernel<BN, AMN, BMN, PRE, EPI>}
+#define TV(AMN, BMN, PRE, EPI) \
+  {AMN, BMN, PRE, EPI, (TcKernel)tc::tc_gemm_kernel<BN, AMN, BMN, PRE, EPI>, tc::Cfg<BN, EPI == EPI_WGRAD>::SMEM}
   static const TcVariant v[] = {
       TV(false, false, true, EPI_FWD),     // forward      Z = A W^T        (weights pre-split)
       TV(false, false, false, EPI_FWD),    // forward, raw weight plane (split in shared memory)
@@ -1012,7 +1061,7 @@ struct TcPlanner {
       int n = 0;
       const TcVariant* v = tc_variants<BN>(&n);
       for (int i = 0; i < n; ++i)
-        cudaFuncSetAttribute((const void*)v[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Cfg<BN>::SMEM);
+        cudaFuncSetAttribute((const void*)v[i].fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v[i].smem);
       attr_done = true;
     }
     enabled = true;
@@ -1142,7 +1191,7 @@ struct TcPlanner {
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(tc::NT);
-    cfg.dynamicSmemBytes = tc::Cfg<BN>::SMEM;
+    cfg.dynamicSmemBytes = v->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -22,3 +22,10 @@ for j in range(0, 24):
     print(f"{j:3d} " + " ".join(f"{(tl[i, j] - t0) if tl[i, j] else 0:10d}" for i in range(8)))
 d = np.diff(tl[3, 8:120])
 print("issue period median", np.median(d))
+# converter warp 0, per K block: A landed -> A split -> slot free -> TMEM st issued -> B landed ->
+# B split -> st done -> fence -> arrive (clocks between consecutive phases)
+ph = ["A_split", "slot", "st_iss", "B_wait", "B_split", "st_done", "fence", "arrive", "->nextA"]
+print("conv0 " + " ".join(f"{n:>8s}" for n in ph))
+for j in range(8, 24):
+    row = [tl[8, j] - tl[6, j]] + [tl[i + 1, j] - tl[i, j] for i in range(8, 15)] + [tl[6, j + 1] - tl[15, j]]
+    print(f"{j:3d}   " + " ".join(f"{v:8d}" for v in row))
