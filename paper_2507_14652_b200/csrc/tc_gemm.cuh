@@ -60,9 +60,9 @@ constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32
 template <int BN, bool WG = false>
 struct Cfg {
   static constexpr int SA = 4;                          // raw A ring (released by the converters)
-  static constexpr int SB = WG ? 5 : 3;                 // B ring (released by the MMA)
+  static constexpr int SB = WG ? 10 : 6;                // B ring (released by the MMA)
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;           // one B plane, 16 KB at BN = 128
+  static constexpr int B_BYTES = (BN / 2) * BK * 4;     // this CTA's half of one B plane, 8 KB
   static constexpr int B_STAGE = 2 * B_BYTES;           // hi + lo planes
 #ifndef TC_NACC
 #define TC_NACC 2
@@ -76,7 +76,8 @@ struct Cfg {
   static constexpr int B_OFF = SA * A_BYTES;
   static constexpr int STG_OFF = B_OFF + SB * B_STAGE;
   static constexpr int STG_BYTES = WG ? 0 : NEPI * NGRP * STG;
-  static constexpr int SMEM = 1024 /*align*/ + STG_OFF + STG_BYTES + 512 /*barriers*/;
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int SMEM = 1024 /*align*/ + STG_OFF + STG_BYTES + BAR_BYTES;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -227,6 +228,52 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* holder, uint32_t cols) {
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
 }
+// CTA-pair TMEM (one warp of each CTA of the pair executes these)
+__device__ __forceinline__ void tmem_alloc2(uint32_t* holder, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(holder)), "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+// pair MMA (issued by the leader CTA only): D (M = 256: 128 rows in each CTA's TMEM) (+)=
+// A (each CTA's TMEM, its 128 rows) . B (N columns: the first N/2 in the leader's shared memory,
+// the rest at the same offset in the peer's)
+__device__ __forceinline__ void mma2_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// pair commit: arrives on the barrier at `bar`'s offset in both CTAs once the leader's prior pair
+// MMAs have completed
+__device__ __forceinline__ void mma2_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the barrier at `b`'s offset in CTA `cta` of the cluster.  Default (release, CTA
+// scope) semantics: a cluster-scope release costs ~1300 clocks (measured) and is not needed -
+// what the leader's MMA consumes is ordered by the tcgen05 fences (TMEM) and the async-proxy
+// fence (shared memory) the arriving warps execute first
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* b, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(b)), "r"(cta));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) { mbar_wait(b, parity); }
+__device__ __forceinline__ void mbar_wait_cl_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
+  if (!on) { mbar_wait_cl(b, parity); return; }
+  const unsigned long long t0 = clock64();
+  mbar_wait_cl(b, parity);
+  acc += clock64() - t0;
+}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accum) {
   asm volatile(
@@ -303,6 +350,7 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // SMEM matrix descriptor, SWIZZLE_128B, sm_100 version bit.
 //  K-major : rows of 128 B (32 fp32 along K), 8-row atoms at SBO = 1024 B, LBO unused (1).
@@ -329,6 +377,10 @@ struct MnDesc {
                  //    CTA-0 timeline of launches of kernel variant v
   int vid = 0;   // kernel variant (index in tc_variants)
   int dbg = 0;   // dev experiments: 1 = no MMAs, 2 = no converter work, 4 = no epilogue fold (results wrong)
+  // raw B planes split in shared memory: hi = the raw word in place (the tensor core reads the
+  // top 19 bits of a tf32 operand, i.e. trunc(x)), lo = rna_tf32(x - trunc(x)) beside it - one
+  // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
+  int btrunc = 1;
 };
 
 // Instruction descriptor for kind::tf32 with fp32 accumulation.
@@ -421,19 +473,21 @@ __global__ void __launch_bounds__(NT, 1)
       mbar_init(&a_empty[s], NCONV);  // one arrive per converter warp
     }
     for (int s = 0; s < SB; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 2);  // both CTAs' MMAs release the (multicast-filled) stage
+      // pre-split planes: the leader's stage is full when its own load and the peer's (relayed)
+      // have landed; raw planes: each CTA's splitters wait for their own half
+      mbar_init(&b_full[s], (B_PRE && crank == 0) ? 2 : 1);
+      mbar_init(&b_empty[s], 1);  // the leader's pair commit, multicast to both CTAs
     }
     for (int i = 0; i < C_::NAS; ++i) {
-      mbar_init(&full_op[i], NCONV);
+      mbar_init(&full_op[i], 2 * NCONV);  // both CTAs' converters arrive on the leader's
       mbar_init(&afree[i], 1);
     }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], NEPI);  // one arrive per epilogue warp
+      mbar_init(&tempty[i], 2 * NEPI);  // one arrive per epilogue warp of both CTAs (on the leader's)
     }
     for (int i = 0; i < NEPI; ++i) mbar_init(&xfull[i], 1);
-    for (int i = 0; i < SB; ++i) mbar_init(&bsplit[i], NEPI);
+    for (int i = 0; i < SB; ++i) mbar_init(&bsplit[i], 2 * NEPI);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tma_prefetch(&mA);
     tma_prefetch(&mB);
@@ -441,7 +495,7 @@ __global__ void __launch_bounds__(NT, 1)
     if (EPI != EPI_WGRAD) tma_prefetch(&mC);
     if (loadx) tma_prefetch(&mX);
   }
-  if (warp == W_MMA) tmem_alloc(tmem_holder, 512);
+  if (warp == W_MMA) tmem_alloc2(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
@@ -486,16 +540,17 @@ __global__ void __launch_bounds__(NT, 1)
           if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
-          // both CTAs of the pair receive the whole B stage: pre-split -> rank r loads plane r;
-          // raw -> rank 0 loads the plane; each multicast to the pair
+          // each CTA of the pair loads its half of the B tile (columns crank * BN/2 ...): the pair
+          // MMA reads the first half from the leader's shared memory, the second from the peer's
           if (mn.dbg & 16) mbar_arrive(&b_full[s]);  // dev experiment: no B traffic
           else {
           mbar_expect_tx(&b_full[s], bytes);
-          if (B_PRE || crank == 0) {
-            uint8_t* dst = (B_PRE && crank == 1) ? sBl : sBh;
-            const CUtensorMap* mp = (B_PRE && crank == 1) ? &mB2 : &mB;
-            if (B_MN) tma_load4_mc(dst, mp, &b_full[s], 0, kb * BK, nt * (BN / 32), b, (uint16_t)3);
-            else tma_load3_mc(dst, mp, &b_full[s], kb * BK, nt * BN, b, (uint16_t)3);
+          const int n_half = nt * BN + (int)crank * (BN / 2);
+          if (B_MN) tma_load4(sBh, &mB, &b_full[s], 0, kb * BK, n_half / 32, b);
+          else tma_load3(sBh, &mB, &b_full[s], kb * BK, n_half, b);
+          if (B_PRE) {
+            if (B_MN) tma_load4(sBl, &mB2, &b_full[s], 0, kb * BK, n_half / 32, b);
+            else tma_load3(sBl, &mB2, &b_full[s], kb * BK, n_half, b);
           }
           }
           if (++s == SB) { s = 0; ph ^= 1; }
@@ -508,8 +563,9 @@ __global__ void __launch_bounds__(NT, 1)
     // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
     // ones Ah.Bh.  The whole warp runs the loop (all values warp-uniform, so they live in uniform
     // registers); one elected lane issues the MMAs and commits.
-    {
-      constexpr uint32_t IDESC = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
+    if (crank == 0) {
+      // leader: pair MMAs M = 256 (128 rows per CTA) x N = BN
+      constexpr uint32_t IDESC = idesc_tf32(2 * BM, BN, 0, B_MN ? 1 : 0);
       const uint32_t b_lbo = B_MN ? mn.lbo : 16, b_sbo = B_MN ? mn.sbo : 1024, b_lay = B_MN ? mn.layout : 2;
       // descriptor of stage 0's B hi plane; the address field (bits 0-13, addr >> 4) is advanced
       // by adding byte offsets >> 4 (all shared addresses < 256 KB)
@@ -525,12 +581,12 @@ __global__ void __launch_bounds__(NT, 1)
           const uint32_t buf = jb % NACC;
           const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
-          mbar_wait_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
+          mbar_wait_cl_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
           if (tl) g_tctl[1][jb] = clock64();
           tc_fence_after();
-          mbar_wait_t(&full_op[jb % C_::NAS], (jb / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
-          if (B_PRE) mbar_wait(&b_full[s], ph);  // (raw B planes are waited for by their splitters)
-          if (ESPLIT) mbar_wait(&bsplit[s], ph);
+          mbar_wait_cl_t(&full_op[jb % C_::NAS], (jb / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
+          if (B_PRE) mbar_wait_cl(&b_full[s], ph);  // (raw B planes are waited for by their splitters)
+          if (ESPLIT) mbar_wait_cl(&bsplit[s], ph);
           if (tl) g_tctl[2][jb] = clock64();
           tc_fence_after();
           const uint32_t dcol = tmem_base + buf * BN;
@@ -542,21 +598,29 @@ __global__ void __launch_bounds__(NT, 1)
             if (!(mn.dbg & 1)) {
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              mma_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, kk == 0 ? 0u : 1u);
-              mma_tf32_ts(dcol, aH + 8 * kk, dBl + kk * kstep16, IDESC, 1u);
+              mma2_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, kk == 0 ? 0u : 1u);
+              mma2_tf32_ts(dcol, aH + 8 * kk, dBl + kk * kstep16, IDESC, 1u);
             }
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) mma_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) mma2_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
             }
-            mma_commit_mc(&b_empty[s], (uint16_t)3);
-            mma_commit(&afree[jb % C_::NAS]);
-            mma_commit(&tfull[buf]);
+            mma2_commit_mc(&b_empty[s]);
+            mma2_commit_mc(&afree[jb % C_::NAS]);
+            mma2_commit_mc(&tfull[buf]);
           }
           __syncwarp();
           if (mn.prof) pacc[2] += clock64() - t_i0;
           if (tl) g_tctl[3][jb] = clock64();
         }
       }
+    } else if (B_PRE && warp == W_MMA && lane == 0) {
+      // peer: relay "my half of the pre-split B stage landed" to the leader's b_full
+      uint32_t jb = 0;
+      for (int t = cid; t < total; t += ncl)
+        for (int kb = 0; kb < nk; ++kb, ++jb) {
+          mbar_wait(&b_full[jb % SB], (jb / SB) & 1u);
+          mbar_arrive_cta(&b_full[jb % SB], 0);
+        }
     }
   } else if (warp >= W_CONV0) {
     // ================================ converters ==================================
@@ -624,6 +688,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll 4
           for (int i = ct; i < ((mn.dbg & 64) ? 0 : C_::B_BYTES / 16); i += NCONV * 32) {  // 64: dev experiment
             float4 x = bh[i];
+            if (mn.btrunc && !(EPI == EPI_WGRAD && a.sq)) {
+              float4 l;
+              l.x = tf32_rna(x.x - tf32_trunc(x.x)); l.y = tf32_rna(x.y - tf32_trunc(x.y));
+              l.z = tf32_rna(x.z - tf32_trunc(x.z)); l.w = tf32_rna(x.w - tf32_trunc(x.w));
+              bl[i] = l;
+              continue;
+            }
             if (EPI == EPI_WGRAD && a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
             float4 h, l;
             h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
@@ -644,7 +715,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (tc0) g_tctl[14][jb] = clock64();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&full_op[as]);
+          mbar_arrive_cta(&full_op[as], 0);
           mbar_arrive(&a_empty[sa]);
         }
         if (tc0) g_tctl[15][jb] = clock64();
@@ -746,6 +817,13 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = ew * 32 + lane; i < C_::B_BYTES / 16; i += NEPI * 32) {
           float4 x = bh[i];
+          if (mn.btrunc && !a.sq) {
+            float4 l;
+            l.x = tf32_rna(x.x - tf32_trunc(x.x)); l.y = tf32_rna(x.y - tf32_trunc(x.y));
+            l.z = tf32_rna(x.z - tf32_trunc(x.z)); l.w = tf32_rna(x.w - tf32_trunc(x.w));
+            bl[i] = l;
+            continue;
+          }
           if (a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
           float4 h, l;
           h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
@@ -755,7 +833,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         fence_proxy_async();  // generic-proxy writes -> the tensor core's async-proxy reads
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bsplit[s]);
+        if (lane == 0) mbar_arrive_cta(&bsplit[s], 0);
       }
     };
     if (ESPLIT) split_upto(ESPLIT_D);
@@ -808,7 +886,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) mbar_arrive_cta(&tempty[buf], 0);
         if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
         if (ESPLIT) split_upto(jb + 1 + ESPLIT_D);
         if (pend > 0) {  // one step of the parked tile per K block
@@ -982,7 +1060,7 @@ __global__ void __launch_bounds__(NT, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // no CTA leaves while its peer may still multicast into it or arrive on it
-  if (warp == W_MMA) tmem_dealloc(tmem_base, 512);
+  if (warp == W_MMA) tmem_dealloc2(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------------- host side ---
@@ -1056,6 +1134,7 @@ struct TcPlanner {
     if (const char* f = getenv("HMC_TC_PF")) mn.pf = std::max(0, atoi(f));
     if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
+    if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
@@ -1168,13 +1247,13 @@ struct TcPlanner {
     bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM, true)
                   : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
     if (pre) {
-      ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, BN)
-                      : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, BN));
-      ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, BN)
-                      : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, BN));
-    } else {
-      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, BN)
-                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, BN));
+      ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, BN / 2)
+                      : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, BN / 2));
+      ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, BN / 2)
+                      : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, BN / 2));
+    } else {  // (each CTA of the pair loads half of the B tile)
+      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, BN / 2)
+                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, BN / 2));
       mB2 = mB;
     }
     if (a.epi != EPI_WGRAD) ok = ok && map_store(&mC, a.C, a.M, a.N, a.ldc, a.sC, a.batch);
