@@ -238,10 +238,12 @@ int hmc_profile_read(hmc_ctx* ctx, int32_t max_recs, hmc_prof_rec* out, int32_t*
  * accumulator, epilogue waiting for prefetched tiles, epilogue output cycles, kernel cycles);
  * reset != 0 zeroes them.  Returns HMC_E_CUDA on a CUDA error. */
 int hmc_debug_tc_profile(uint64_t* out, int32_t reset);
-/* With HMC_TC_PROF=2: clock64 timeline of CTA 0 of the most recent tensor-core GEMM, out[16 x 256]
+/* With HMC_TC_PROF=2: clock64 timeline of CTA 0 of the most recent tensor-core GEMM, out[24 x 256]
  * (host): per K block, MMA loop top / accumulator free / operands ready / issued, epilogue
  * partial ready / folded, converter A landed / operands published; rows 8-15: phases of converter
- * warp 0 (A split, slot free, TMEM store issued, B landed, B split, store done, fence, arrive). */
+ * warp 0 (A split, slot free, TMEM store issued, B landed, B split, store done, fence, arrive);
+ * rows 16-22: epilogue warp 0 (partial ready, folded, released, emitted; at the tile end: flushed,
+ * biased / prefetch landed, parked). */
 int hmc_debug_tc_timeline(uint64_t* out);
 
 #ifdef __cplusplus

@@ -236,12 +236,12 @@ def hmc_debug_tc_profile(reset: bool = False):
 
 
 def hmc_debug_tc_timeline():
-    """CTA-0 timeline [16 x 256] (clock64) of the last tcgen05 GEMM with HMC_TC_PROF=2."""
-    out = (ctypes.c_uint64 * (16 * 256))()
+    """CTA-0 timeline [24 x 256] (clock64) of the last tcgen05 GEMM with HMC_TC_PROF=2."""
+    out = (ctypes.c_uint64 * (24 * 256))()
     L = lib()
     L.hmc_debug_tc_timeline.argtypes = [ctypes.c_void_p]
     _check(L.hmc_debug_tc_timeline(out))
-    return np.array(list(out), dtype=np.int64).reshape(16, 256)
+    return np.array(list(out), dtype=np.int64).reshape(24, 256)
 
 
 def hmc_profile(ctx, enable: bool):

@@ -1448,9 +1448,9 @@ int hmc_debug_tc_profile(uint64_t* out, int32_t reset) {
   return HMC_OK;
 }
 
-// dev diagnostics: CTA-0 timeline of the last tcgen05 GEMM run with HMC_TC_PROF=2, out[16 x 256]
+// dev diagnostics: CTA-0 timeline of the last tcgen05 GEMM run with HMC_TC_PROF=2, out[24 x 256]
 int hmc_debug_tc_timeline(uint64_t* out) {
-  if (cudaMemcpyFromSymbol(out, tc::g_tctl, sizeof(unsigned long long) * 16 * tc::TL_N) != cudaSuccess) return HMC_E_CUDA;
+  if (cudaMemcpyFromSymbol(out, tc::g_tctl, sizeof(unsigned long long) * 24 * tc::TL_N) != cudaSuccess) return HMC_E_CUDA;
   return HMC_OK;
 }
 

@@ -142,7 +142,7 @@ __device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
 // 2 full_op ok, 3 issued, 4 epilogue tfull ok, 5 epilogue folded, 6 converter full (A) ok,
 // 7 converter arrive full_op
 constexpr int TL_N = 256;
-__device__ unsigned long long g_tctl[16][TL_N];
+__device__ unsigned long long g_tctl[24][TL_N];
 __device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
   if (!on) { mbar_wait(b, parity); return; }
   const unsigned long long t0 = clock64();
@@ -648,13 +648,15 @@ __global__ void __launch_bounds__(NT, 1)
           for (int q = 0; q < 8; ++q) {
             float4 x = row[q ^ (r & 7)];
             if (EPI == EPI_WGRAD && a.sq) { x.x *= x.x; x.y *= x.y; x.z *= x.z; x.w *= x.w; }
-            const float xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float h = tf32_rna(xv[e]);
-              hi[4 * q + e] = __float_as_uint(h);
-              lo[4 * q + e] = __float_as_uint(xv[e] - h);
-            }
+            // lo = x - hi on packed pairs (FADD2: half the issue slots)
+            const float h0 = tf32_rna(x.x), h1 = tf32_rna(x.y), h2 = tf32_rna(x.z), h3 = tf32_rna(x.w);
+            hi[4 * q + 0] = __float_as_uint(h0); hi[4 * q + 1] = __float_as_uint(h1);
+            hi[4 * q + 2] = __float_as_uint(h2); hi[4 * q + 3] = __float_as_uint(h3);
+            float l0, l1, l2, l3;
+            upk2(fadd2(pk2(x.x, x.y), pk2(-h0, -h1)), l0, l1);
+            upk2(fadd2(pk2(x.z, x.w), pk2(-h2, -h3)), l2, l3);
+            lo[4 * q + 0] = __float_as_uint(l0); lo[4 * q + 1] = __float_as_uint(l1);
+            lo[4 * q + 2] = __float_as_uint(l2); lo[4 * q + 3] = __float_as_uint(l3);
           }
         } else {  // [m / 32][k][m % 32], no swizzle: lanes read consecutive words
           const float* col = (const float*)stA + (r >> 5) * 1024 + (r & 31);
@@ -745,9 +747,11 @@ __global__ void __launch_bounds__(NT, 1)
     // with 8 K blocks per tile the last store is issued two folds before the tile end, so its
     // read of the staging tile has completed when the next tile is parked
     const int nstep = (EPI == EPI_FWD && a.act == ACT_TANH) ? 3 : 1;
+    bool tstep = false;  // timeline: stamp the end of the emit step's register work (row 23)
+    uint32_t tstep_j = 0;
     auto emit_step = [&](int k) {
       if (mn.dbg & 8) return;  // dev experiment: no output traffic
-      const int g = k / nstep, part = k - g * nstep;
+      const int g = (nstep == 3) ? k / 3 : k, part = k - g * nstep;
       uint8_t* stg = stg0 + g * STG;
       float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
       const int n0 = p_nb + 32 * g;
@@ -762,6 +766,7 @@ __global__ void __launch_bounds__(NT, 1)
           srow[q ^ (lane & 7)] = z;
         }
       }
+      if (tstep) g_tctl[23][tstep_j] = clock64();
       if (part != nstep - 1) return;
       fence_proxy_async();
       __syncwarp();
@@ -870,6 +875,8 @@ __global__ void __launch_bounds__(NT, 1)
         const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
         const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
+        const bool te = tl && blockIdx.x == 0;  // epilogue warp 0 phase stamps
+        if (te) g_tctl[16][jb] = clock64();
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
@@ -879,19 +886,25 @@ __global__ void __launch_bounds__(NT, 1)
           tmem_ld16(taddr + c0 + 16, r1);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            acc[c0 + i] += __uint_as_float(r0[i]);
-            acc[c0 + 16 + i] += __uint_as_float(r1[i]);
+          for (int i = 0; i < 16; i += 2) {  // packed pairs (FADD2: half the issue slots)
+            upk2(fadd2(pk2(acc[c0 + i], acc[c0 + i + 1]), pk2(__uint_as_float(r0[i]), __uint_as_float(r0[i + 1]))),
+                 acc[c0 + i], acc[c0 + i + 1]);
+            upk2(fadd2(pk2(acc[c0 + 16 + i], acc[c0 + 17 + i]), pk2(__uint_as_float(r1[i]), __uint_as_float(r1[i + 1]))),
+                 acc[c0 + 16 + i], acc[c0 + 17 + i]);
           }
         }
+        if (te) g_tctl[17][jb] = clock64();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&tempty[buf], 0);
         if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
+        if (te) g_tctl[18][jb] = clock64();
         if (ESPLIT) split_upto(jb + 1 + ESPLIT_D);
         if (pend > 0) {  // one step of the parked tile per K block
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
+          tstep = te; tstep_j = jb;
           emit_step(p_next++);
+          tstep = false;
           if (--pend == 0 && loadx && !prefetched) {
             staging_free();
             issue_prefetch(b, mt, nt);
@@ -899,7 +912,9 @@ __global__ void __launch_bounds__(NT, 1)
           }
           if (mn.prof) pacc[2] += clock64() - t_e0;
         }
+        if (te) g_tctl[19][jb] = clock64();
       }
+      const bool tt = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb - 1 < TL_N && lane == 0 && ew == 0;
       const unsigned long long t_out0 = mn.prof ? clock64() : 0ull;
       while (pend > 0) {  // short K: flush the parked tile
         emit_step(p_next++);
@@ -910,12 +925,14 @@ __global__ void __launch_bounds__(NT, 1)
         issue_prefetch(b, mt, nt);
       }
       if (!loadx) staging_free();
+      if (tt) g_tctl[20][jb - 1] = clock64();
       if (EPI == EPI_FWD) {  // + bias (column u*32 + l lives in lane l's bias_l[u])
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] += __shfl_sync(0xffffffffu, bias_l[i >> 5], i & 31);
       }
       // ---- tile end: the register part of the fused epilogue, parked in staging ----
       if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
+      if (tt) g_tctl[21][jb - 1] = clock64();
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
@@ -1015,6 +1032,7 @@ __global__ void __launch_bounds__(NT, 1)
         p_blk = mt * 4 + quad;
         __syncwarp();
       }
+      if (tt) g_tctl[22][jb - 1] = clock64();
       if (mn.prof) pacc[2] += clock64() - t_out0;
       if (EPI == EPI_RESID) {
         // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps

@@ -29,3 +29,14 @@ print("conv0 " + " ".join(f"{n:>8s}" for n in ph))
 for j in range(8, 24):
     row = [tl[8, j] - tl[6, j]] + [tl[i + 1, j] - tl[i, j] for i in range(8, 15)] + [tl[6, j + 1] - tl[15, j]]
     print(f"{j:3d}   " + " ".join(f"{v:8d}" for v in row))
+# epilogue warp 0, per K block: partial ready -> folded -> released -> emitted -> next ready
+print("epi0    wait_tf     fold  release  emit_rg emit_out")
+for j in range(8, 24):
+    w = tl[16, j] - tl[19, j - 1]
+    er = (tl[23, j] - tl[18, j]) if tl[23, j] else 0
+    eo = (tl[19, j] - tl[23, j]) if tl[23, j] else tl[19, j] - tl[18, j]
+    print(f"{j:3d}   " + " ".join(f"{v:8d}" for v in [w, tl[17, j] - tl[16, j], tl[18, j] - tl[17, j], er, eo]))
+print("tile ends (kb, flush, bias/xfull, park):")
+for j in range(0, 64):
+    if tl[20, j]:
+        print(f"{j:3d}   {tl[20, j] - tl[19, j]:8d} {tl[21, j] - tl[20, j]:8d} {tl[22, j] - tl[21, j]:8d}")
