@@ -56,7 +56,8 @@ class Problem:
 
     Arrays are float32 (the canonical inputs); idx is int32,
     strictly ascending.  For 'mlp': x [n, d_in], y [n].  For 'deeponet':
-    u [n_c, m] (branch inputs), q [n_x, d_t] (trunk inputs), v [n_c, n_x].
+    u [n_c, m] (branch inputs), q [n_x, d_t] (trunk inputs; unaligned DeepONet: q [n_c, n_x, d_t],
+    each pair its own query point), v [n_c, n_x].
     """
 
     name: str

@@ -120,7 +120,9 @@ def make_problem(name: str, n_chains: Optional[int] = None) -> Problem:
     """Build one of cfg1..cfg5 or 'blr' exactly per SURVEY §8(d)."""
     if name == "blr":
         return make_blr_problem(n_chains or 4)
-    spec = CONFIGS[name]
+    # cfg4u: cfg4 with the query points drawn per function (unaligned DeepONet, NEXT-4, Q16)
+    unaligned = name == "cfg4u"
+    spec = CONFIGS["cfg4" if unaligned else name]
     cid = spec["cid"]
     arch: ArchSpec = spec["arch"]
     P = n_params(arch)
@@ -151,6 +153,14 @@ def make_problem(name: str, n_chains: Optional[int] = None) -> Problem:
         x = rng(3, 0).normal(size=(spec["n"], 8))
         y = _teacher(x, rng(3, 4)) + rng(3, 1).normal(0.0, noise, size=spec["n"])
         return Problem(x=x.astype(np.float32), y=y.astype(np.float32), **kw)
+    if unaligned:
+        s = np.arange(100) / 99.0
+        u = _grf_rbf(spec["n_c"], s, 0.2, rng(4, 4))
+        yq = rng(4, 6).uniform(0.0, 1.0, size=(spec["n_c"], spec["n_x"]))
+        G = np.stack([_antiderivative_pl(u[c:c + 1], s, yq[c])[0] for c in range(spec["n_c"])])
+        v = G + rng(4, 1).normal(0.0, noise, size=(spec["n_c"], spec["n_x"]))
+        return Problem(u=u.astype(np.float32), q=yq[:, :, None].astype(np.float32),
+                       v=v.astype(np.float32), **kw)
     if name == "cfg4":
         s = np.arange(100) / 99.0
         u = _grf_rbf(spec["n_c"], s, 0.2, rng(4, 4))
@@ -189,7 +199,8 @@ def make_blr_problem(n_chains: int = 4) -> Problem:
 def make_tiny_problem(arch: ArchSpec, *, n: int = 0, n_c: int = 0, n_x: int = 0,
                       active_frac: float = 1.0, n_chains: int = 1, seed: int = 0,
                       noise: float = 0.1, prior: float = 1.0, mu_scale: float = 0.5,
-                      inv_mass: bool = False, L: int = 10, eps: float = 1e-3) -> Problem:
+                      inv_mass: bool = False, L: int = 10, eps: float = 1e-3,
+                      unaligned: bool = False) -> Problem:
     """Small seeded problems for pins and parity tests (any arch, ragged sizes)."""
     g = np.random.default_rng(np.random.SeedSequence([1000 + seed, 0]))
     P = n_params(arch)
@@ -209,6 +220,6 @@ def make_tiny_problem(arch: ArchSpec, *, n: int = 0, n_c: int = 0, n_x: int = 0,
     m = arch.nets[0].widths[0]
     dt = arch.nets[1].widths[0]
     u = g.normal(size=(n_c, m)).astype(np.float32)
-    q = g.uniform(0.0, 1.0, size=(n_x, dt)).astype(np.float32)
+    q = g.uniform(0.0, 1.0, size=((n_c, n_x, dt) if unaligned else (n_x, dt))).astype(np.float32)
     v = g.normal(size=(n_c, n_x)).astype(np.float32)
     return Problem(u=u, q=q, v=v, **kw)

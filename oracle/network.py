@@ -6,6 +6,10 @@ sin / tanh), P:369 + P:527-539 (DeepONet: branch and trunk are feed-forward nets
 DeepONet output F(u, y) = sum_k B_k(u) T_k(y) + b0.
 Flat layout (SURVEY §2.3 D1): per net, per layer W[out x in] row-major then b[out];
 DeepONet b0 last.
+Unaligned DeepONet: the query points differ per function, data["q"]
+is [n_c, n_x, d_t] and pair (c, x) is F(u_c, y_{c,x}) - the same definition with the
+trunk evaluated on every pair's own point (n_c * n_x trunk inputs); the aligned layout
+q [n_x, d_t] shares the points across functions (trunk on n_x inputs).
 """
 from __future__ import annotations
 
@@ -91,6 +95,35 @@ def net_backward(arch, theta_full, ni, tape, dout, grad_full):
     return g
 
 
+def _unaligned(data):
+    return np.asarray(data["q"]).ndim == 3
+
+
+def _trunk_inputs(data):
+    """Trunk input rows: q [n_x, d_t] (aligned) or q [n_c, n_x, d_t] flattened pair-major."""
+    q = np.asarray(data["q"], dtype=np.float64)
+    return q.reshape(-1, q.shape[-1]) if q.ndim == 3 else q
+
+
+def _combine(B, T, data):
+    """Sum_k B_ck T_(pair)k for every pair: B T^T (aligned) or row-wise dots (unaligned)."""
+    if not _unaligned(data):
+        return B @ T.T
+    n_c, n_x = np.asarray(data["q"]).shape[:2]
+    return np.einsum("ck,cxk->cx", B, T.reshape(n_c, n_x, -1))
+
+
+def _combine_grads(B, T, E, data):
+    """dF-weighted sums: (sum_x E_cx T_(c,x)k  per c,  E_cx B_ck per trunk row)."""
+    if not _unaligned(data):
+        return E @ T, E.T @ B
+    n_c, n_x = E.shape
+    T3 = T.reshape(n_c, n_x, -1)
+    dB = np.einsum("cx,cxk->ck", E, T3)
+    dT = (E[:, :, None] * B[:, None, :]).reshape(n_c * n_x, -1)
+    return dB, dT
+
+
 def predict(arch, theta_full, data):
     """F for every datum: MLP -> [n]; DeepONet -> [n_c, n_x] (each pair (c, x) is
     F(u_c, y_x) = B(u_c) . T(y_x) + b0: branch evaluated once per function, trunk once
@@ -100,9 +133,9 @@ def predict(arch, theta_full, data):
         out, _ = net_forward(arch, theta_full, 0, data["x"])
         return out[:, 0]
     B, _ = net_forward(arch, theta_full, 0, data["u"])
-    T, _ = net_forward(arch, theta_full, 1, data["q"])
+    T, _ = net_forward(arch, theta_full, 1, _trunk_inputs(data))
     _, b0, _ = layer_table(arch)
-    F = B @ T.T
+    F = _combine(B, T, data)
     if b0 is not None:
         F = F + theta_full[b0]
     return F
@@ -137,16 +170,17 @@ def loglik_grad(arch, theta_full, data, sigma):
         net_backward(arch, theta_full, 0, tape, (r / s2)[:, None], grad)
         return ll, grad, r
     B, tb = net_forward(arch, theta_full, 0, data["u"])
-    T, tt = net_forward(arch, theta_full, 1, data["q"])
+    T, tt = net_forward(arch, theta_full, 1, _trunk_inputs(data))
     _, b0, _ = layer_table(arch)
-    F = B @ T.T
+    F = _combine(B, T, data)
     if b0 is not None:
         F = F + theta_full[b0]
     R = np.asarray(data["v"], dtype=np.float64) - F
     ll = -np.sum(R * R) / (2.0 * s2)
     E = R / s2                       # d ll / d F
-    net_backward(arch, theta_full, 0, tb, E @ T, grad)     # dF/dB_ck = T_xk
-    net_backward(arch, theta_full, 1, tt, E.T @ B, grad)   # dF/dT_xk = B_ck
+    dB, dT = _combine_grads(B, T, E, data)
+    net_backward(arch, theta_full, 0, tb, dB, grad)     # dF/dB_ck = T_(pair)k
+    net_backward(arch, theta_full, 1, tt, dT, grad)     # dF/dT_(pair)k = B_ck
     if b0 is not None:
         grad[b0] += E.sum()
     return ll, grad, R
@@ -196,11 +230,12 @@ def grad_abs_scale(arch, theta_full, data, sigma):
         bwd(0, tape, seed[:, None])
         return S
     B, tb = fwd(0, data["u"])
-    T, tt = fwd(1, data["q"])
-    F = B @ T.T + (np.asarray(theta_full, dtype=np.float64)[b0] if b0 is not None else 0.0)
+    T, tt = fwd(1, _trunk_inputs(data))
+    F = _combine(B, T, data) + (np.asarray(theta_full, dtype=np.float64)[b0] if b0 is not None else 0.0)
     E = (np.abs(F) + np.abs(np.asarray(data["v"], dtype=np.float64))) / s2
-    bwd(0, tb, E @ np.abs(T))
-    bwd(1, tt, E.T @ np.abs(B))
+    dB, dT = _combine_grads(np.abs(B), np.abs(T), E, data)
+    bwd(0, tb, dB)
+    bwd(1, tt, dT)
     if b0 is not None:
         S[b0] += E.sum()
     return S

@@ -41,17 +41,19 @@ def output_grad_per_datum(arch, theta_full, data):
     _, b0, _ = layer_table(arch)
     u = np.asarray(data["u"], dtype=np.float64)
     q = np.asarray(data["q"], dtype=np.float64)
+    n_x = q.shape[1] if q.ndim == 3 else q.shape[0]   # unaligned: q [n_c, n_x, d_t]
     for c in range(u.shape[0]):
         B, tb = net_forward(arch, theta_full, 0, u[c:c + 1])
-        for xi in range(q.shape[0]):
-            T, tt = net_forward(arch, theta_full, 1, q[xi:xi + 1])
+        for xi in range(n_x):
+            qp = q[c, xi:xi + 1] if q.ndim == 3 else q[xi:xi + 1]
+            T, tt = net_forward(arch, theta_full, 1, qp)
             g = np.zeros(P)
             # F = sum_k B_k T_k + b0: dF/dB_k = T_k, dF/dT_k = B_k, dF/db0 = 1
             net_backward(arch, theta_full, 0, tb, T, g)
             net_backward(arch, theta_full, 1, tt, B, g)
             if b0 is not None:
                 g[b0] += 1.0
-            yield c * q.shape[0] + xi, g
+            yield c * n_x + xi, g
 
 
 def sensitivities(arch, mu, sigma_vi, data):
