@@ -74,8 +74,12 @@ typedef struct {
 /* Training data D, fp32 row-major, host or device; copied in at setup, the caller may
  * free it on return.  MLP: x[n x d_in], y[n].  DeepONet (cartesian product layout, Q16):
  * u[n_c x m] branch inputs (function samples at the sensors), q[n_x x d_t] trunk inputs,
- * v[n_c x n_x] targets, pair (c, x) -> v[c * n_x + x].  In data mode these are this rank's
- * shard (a row block of x/y, or of u/v for a DeepONet); n_global is the sum over ranks. */
+ * v[n_c x n_x] targets, pair (c, x) -> v[c * n_x + x].  q_per_pair = 1 selects the unaligned
+ * DeepONet: every pair has its own query point, q[n_c x n_x x d_t]
+ * (pair (c, x) -> row c * n_x + x), the trunk runs on all n_c * n_x points and the combine is a
+ * row-wise dot (P:369 DeepONets).  In data mode these are this rank's
+ * shard (a row block of x/y, or of u/v (and q when unaligned) for a DeepONet); n_global is the
+ * sum over ranks. */
 typedef struct {
   const float* x;
   const float* y;
@@ -85,6 +89,7 @@ typedef struct {
   const float* v;
   int64_t n_c, n_x;
   int64_t n_global;
+  int32_t q_per_pair; /* DeepONet: 0 = q[n_x x d_t] shared by all functions, 1 = q[n_c x n_x x d_t] */
 } hmc_data;
 
 typedef struct {

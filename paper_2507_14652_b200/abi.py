@@ -39,7 +39,8 @@ class hmc_arch(ctypes.Structure):
 class hmc_data(ctypes.Structure):
     _fields_ = [("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("n", ctypes.c_int64),
                 ("u", ctypes.c_void_p), ("q", ctypes.c_void_p), ("v", ctypes.c_void_p),
-                ("n_c", ctypes.c_int64), ("n_x", ctypes.c_int64), ("n_global", ctypes.c_int64)]
+                ("n_c", ctypes.c_int64), ("n_x", ctypes.c_int64), ("n_global", ctypes.c_int64),
+                ("q_per_pair", ctypes.c_int32)]
 
 
 class hmc_config(ctypes.Structure):
@@ -317,7 +318,8 @@ def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):
         d.u = _ptr(problem.u, keep, np.float32)
         d.q = _ptr(problem.q, keep, np.float32)
         d.v = _ptr(problem.v, keep, np.float32)
-        d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.q.shape[0])
+        d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.v.shape[1])
+        d.q_per_pair = int(len(problem.q.shape) == 3)  # unaligned: q [n_c, n_x, d_t]
     mu = problem.frozen if mu is None else mu
     sigma_vi = problem.sigma_vi if sigma_vi is None else sigma_vi
     P = int(np.asarray(mu).shape[0]) if not hasattr(mu, "device") else int(mu.shape[0])
@@ -351,7 +353,8 @@ class Context:
             d.u = _ptr(problem.u, keep, np.float32)
             d.q = _ptr(problem.q, keep, np.float32)
             d.v = _ptr(problem.v, keep, np.float32)
-            d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.q.shape[0])
+            d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.v.shape[1])
+            d.q_per_pair = int(len(problem.q.shape) == 3)  # unaligned: q [n_c, n_x, d_t]
         d.n_global = int(n_global)
         c = hmc_config()
         c.frozen = _ptr(problem.frozen, keep, np.float32)

@@ -65,6 +65,7 @@ struct hmc_ctx {
   int dev = 0, kind = 0, C = 0, mode = 0, rank = 0, world = 1;
   int64_t P = 0, k = 0;
   int64_t n = 0, n_c = 0, n_x = 0, n_global = 0, d_in = 0;
+  bool unaligned = false;  // DeepONet with per-pair trunk inputs q[n_c x n_x x d_t] (NEXT-4)
   double sigma = 1, sigma_p = 1;
   uint64_t seed = 0;
   bool has_b0 = false;
@@ -479,6 +480,30 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   const LayerInfo& Bl = x->layers[Nb.layers.back()];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Bl.n_out;
+  if (x->unaligned) {  // per-pair trunk rows: row-wise combine, then the two output gradients
+    k_pair_combine<<<dim3((unsigned)x->n_c, C), 256, p * sizeof(float), st>>>(
+        Bl.A, Tl.A, p, x->n_c, x->n_x, x->d_v, x->has_b0 ? x->Wd + x->b0_off : nullptr, x->P,
+        1.0 / (x->sigma * x->sigma), x->R, x->part_sq, x->part_r, x->n_part);
+    x->launches++;
+    x->flop_acc += 2.0 * C * x->n_c * x->n_x * p;
+    if (Nb.l_min >= 0) {
+      k_pair_dB<<<dim3((unsigned)x->n_c, C), 256, 0, st>>>(x->R, Tl.A, p, x->n_c, x->n_x, Bl.act, Bl.A, Bl.D,
+                                                           Nb.G[0]);
+      x->launches++;
+      Nb.cs_ready = false;
+    }
+    if (Nt.l_min >= 0) {
+      const int64_t total = (int64_t)C * x->n_c * x->n_x * p;
+      k_pair_dT<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+          x->R, Bl.A, p, x->n_c, x->n_x, C, Tl.act, Tl.A, Tl.D, Nt.G[0]);
+      x->launches++;
+      Nt.cs_ready = false;
+    }
+    x->flop_acc += 4.0 * C * x->n_c * x->n_x * p;
+    if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+    if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    return;
+  }
   {  // combine O = B T^T + b0, residual, R = (V - O)/sigma^2, partial sums
     GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
     a.A = Bl.A; a.lda = p; a.sA = x->n_c * p;
@@ -849,14 +874,16 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     CFG(data->u && data->q && data->v && data->n_c >= 1 && data->n_x >= 1, "DeepONet data needs u, q, v, n_c, n_x >= 1");
     x->n_c = data->n_c;
     x->n_x = data->n_x;
+    x->unaligned = data->q_per_pair != 0;
+    const int64_t q_rows = x->unaligned ? x->n_c * x->n_x : x->n_x;
     hu = to_host(data->u, (size_t)(x->n_c * arch->net[0].widths[0]), err);
-    hq = to_host(data->q, (size_t)(x->n_x * arch->net[1].widths[0]), err);
+    hq = to_host(data->q, (size_t)(q_rows * arch->net[1].widths[0]), err);
     hv = to_host(data->v, (size_t)(x->n_c * x->n_x), err);
     for (float v : hu) CFG(std::isfinite(v), "u must be finite");
     for (float v : hq) CFG(std::isfinite(v), "q must be finite");
     for (float v : hv) CFG(std::isfinite(v), "v must be finite");
     x->nets[0].rows = x->n_c;
-    x->nets[1].rows = x->n_x;
+    x->nets[1].rows = q_rows;
   }
   const int64_t n_local = x->kind == HMC_MLP ? x->n : x->n_c * x->n_x;
   x->n_global = data->n_global > 0 ? data->n_global : n_local;
@@ -964,9 +991,10 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     probe.epi = EPI_RESID;
     probe.lda = p; probe.sA = x->n_c * p; probe.ldb = p; probe.sB = x->n_x * p;
     const int bm = pick_bm((int)x->n_c, (int)x->n_x);
-    // partial slots: max over both engines (unused slots stay zero)
-    x->n_part = std::max(x->tc.n_tiles(probe, true, true),
-                         (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
+    // partial slots: max over both engines (unused slots stay zero); unaligned: one per function
+    x->n_part = x->unaligned ? (int)x->n_c
+                             : std::max(x->tc.n_tiles(probe, true, true),
+                                        (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
   }
   {  // two-pass column-reduction scratch: max over nets of chunks x (width + 1)
     size_t cap = 0;
@@ -1239,12 +1267,17 @@ int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, dou
       const LayerInfo& Bl = x->layers[x->nets[0].layers.back()];
       const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
       const int p = Bl.n_out;
-      GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
-      a.A = Bl.A; a.lda = p; a.sA = x->n_c * p;
-      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-      a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
-      a.epi = EPI_STORE;
-      launch_gemm(x, a, true, true, x->st, "predict");
+      if (x->unaligned) {  // F per pair (no residual), b0 added by k_pred_accum
+        k_pair_combine<<<dim3((unsigned)x->n_c, C), 256, p * sizeof(float), x->st>>>(
+            Bl.A, Tl.A, p, x->n_c, x->n_x, nullptr, nullptr, 0, 0.0, x->R, nullptr, nullptr, 0);
+      } else {
+        GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+        a.A = Bl.A; a.lda = p; a.sA = x->n_c * p;
+        a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+        a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+        a.epi = EPI_STORE;
+        launch_gemm(x, a, true, true, x->st, "predict");
+      }
     }
     k_pred_accum<<<148 * 4, 256, 0, x->st>>>(x->R, N, nb, x->Wd, x->P, x->has_b0 ? x->b0_off : -1, dsum, dsq);
     CK(cudaGetLastError());
@@ -1298,6 +1331,9 @@ int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu,
   std::unique_ptr<hmc_ctx> x(new hmc_ctx());
   std::string& err = x->err;
   try {
+    CFG(arch->kind != HMC_DEEPONET || !data->q_per_pair,
+        "hmc_sensitivity: the unaligned DeepONet (q_per_pair) is not supported (its Gram-seed "
+        "factorisation needs shared query points)");
     // P from the architecture (the same walk setup_impl validates)
     int64_t P = 0;
     for (int ni = 0; ni < (arch->kind == HMC_DEEPONET ? 2 : 1); ++ni) {

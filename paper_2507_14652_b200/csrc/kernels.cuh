@@ -659,4 +659,95 @@ __global__ void k_momentum(KState s, uint32_t iter, float* __restrict__ out) {
   }
 }
 
+
+// ================= unaligned DeepONet (per-pair trunk inputs) =================
+// Pair (c, x) has its own trunk row r = c * n_x + x: F_cx = sum_k B_ck T_rk + b0.  The
+// combine is a row-wise dot (no GEMM: each trunk row meets one branch row), read once from HBM.
+
+// act' of a layer output at element t: tanh -> 1 - a^2 (a = output), sin -> D (cos z, stored by
+// the forward), identity -> 1
+__device__ __forceinline__ float dact_at(int act, const float* __restrict__ A, const float* __restrict__ D, int64_t t) {
+  if (act == ACT_TANH) { const float a = A[t]; return 1.f - a * a; }
+  if (act == ACT_SIN) return D[t];
+  return 1.f;
+}
+
+// combine + residual: block (c, chain), one warp per pair row x (lanes over k).  V != nullptr:
+// R_cx = (V_cx - F_cx) / sigma^2 and the fixed-order fp64 partials sum r^2, sum R of the block go
+// to slot c of the chain; V == nullptr (prediction): R_cx = F_cx.
+__global__ void __launch_bounds__(256) k_pair_combine(const float* __restrict__ B, const float* __restrict__ T,
+                                                      int p, int64_t n_c, int64_t n_x,
+                                                      const float* __restrict__ V, const float* __restrict__ b0,
+                                                      int64_t s_b0, double inv_s2, float* __restrict__ R,
+                                                      double* __restrict__ part_sq, double* __restrict__ part_r,
+                                                      int n_part) {
+  extern __shared__ float sBrow[];
+  __shared__ double red[2][8];
+  const int64_t c = blockIdx.x;
+  const int ch = blockIdx.y;
+  const float* Bc = B + ((int64_t)ch * n_c + c) * p;
+  for (int k = threadIdx.x; k < p; k += blockDim.x) sBrow[k] = Bc[k];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float bb = b0 ? b0[(int64_t)ch * s_b0] : 0.f;
+  const float is2 = (float)inv_s2;
+  double sq = 0.0, sr = 0.0;
+  for (int64_t xi = w; xi < n_x; xi += 8) {
+    const float* Tr = T + ((int64_t)ch * n_c * n_x + c * n_x + xi) * p;
+    float d = 0.f;
+    for (int k = lane; k < p; k += 32) d = fmaf(sBrow[k], Tr[k], d);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const float F = d + bb;
+    const int64_t o_idx = ((int64_t)ch * n_c + c) * n_x + xi;
+    if (V) {
+      const float r = V[c * n_x + xi] - F;
+      const float e = r * is2;
+      if (lane == 0) R[o_idx] = e;
+      sq += (double)r * (double)r;
+      sr += (double)e;
+    } else if (lane == 0) {
+      R[o_idx] = F;
+    }
+  }
+  if (!V) return;
+  if (lane == 0) { red[0][w] = sq; red[1][w] = sr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < 8; ++i) { a += red[0][i]; b += red[1][i]; }
+    part_sq[(int64_t)ch * n_part + c] = a;
+    part_r[(int64_t)ch * n_part + c] = b;
+  }
+}
+
+// branch output gradient: G_ck = act'_B(c, k) * sum_x R_cx T_(c n_x + x) k; block (c, chain),
+// threads over k (rows of T read coalesced), fixed-order sum over x
+__global__ void __launch_bounds__(256) k_pair_dB(const float* __restrict__ R, const float* __restrict__ T, int p,
+                                                 int64_t n_c, int64_t n_x, int act, const float* __restrict__ A,
+                                                 const float* __restrict__ D, float* __restrict__ G) {
+  const int64_t c = blockIdx.x;
+  const int ch = blockIdx.y;
+  const float* Rc = R + ((int64_t)ch * n_c + c) * n_x;
+  const float* Tc = T + ((int64_t)ch * n_c * n_x + c * n_x) * p;
+  for (int k = threadIdx.x; k < p; k += blockDim.x) {
+    float s = 0.f;
+    for (int64_t xi = 0; xi < n_x; ++xi) s = fmaf(Rc[xi], Tc[xi * p + k], s);
+    const int64_t t = ((int64_t)ch * n_c + c) * p + k;
+    G[t] = s * dact_at(act, A, D, t);
+  }
+}
+
+// trunk output gradient: G_(c n_x + x) k = R_cx B_ck act'_T(row, k), element-wise
+__global__ void k_pair_dT(const float* __restrict__ R, const float* __restrict__ B, int p, int64_t n_c, int64_t n_x,
+                          int C, int act, const float* __restrict__ A, const float* __restrict__ D,
+                          float* __restrict__ G) {
+  const int64_t rows = n_c * n_x, total = (int64_t)C * rows * p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t % p, rr = t / p;     // rr = chain * rows + c * n_x + x
+    const int64_t ch = rr / rows, row = rr - ch * rows, c = row / n_x;
+    G[t] = R[rr] * B[(ch * n_c + c) * p + k] * dact_at(act, A, D, t);
+  }
+}
+
 }  // namespace hmc

@@ -41,7 +41,7 @@ def test_struct_layouts_match_header():
     # hmc_net: int32 + 3 pointers (padded) ; hmc_arch: kind + 2 nets + has_b0
     assert ctypes.sizeof(abi.hmc_net) == 32
     assert abi.hmc_arch.net.offset == 8
-    assert ctypes.sizeof(abi.hmc_data) == 9 * 8
+    assert ctypes.sizeof(abi.hmc_data) == 10 * 8 and abi.hmc_data.q_per_pair.offset == 9 * 8
     assert abi.hmc_config.nccl_id.offset == ctypes.sizeof(abi.hmc_config) - 8
 
 
