@@ -34,6 +34,8 @@ WORKLOAD_DESC = {
     "cfg3": "cfg3 MLP 8-256x3-1 tanh, 134,145 params, 6,707 active, N=16384",
     "cfg4": "cfg4 DeepONet branch 100-128-128-128-100 / trunk 1-128-128-100, 88,521 params, 8,852 active, 1000x100 pairs",
     "cfg5": "cfg5 cone-surface DeepONet branch 5-256x5 / trunk 2-256x5, 528,641 params, 20,000 active, 512x2048 pairs",
+    "cfg4u": "cfg4u unaligned DeepONet (cfg4 nets, per-function query points: trunk on 100,000 inputs per "
+             "chain), 88,521 params, 8,852 active, 1000x100 pairs",
 }
 
 

@@ -100,7 +100,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 //              1: try_wait with a short suspend-time hint, so a sleeping waiter re-checks soon
 //                 after an async-proxy completion (tcgen05.commit / TMA complete_tx);
 //              2: test_wait spin (no suspension)
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, uint32_t hint = 20) {
 #if TC_WAIT_MODE == 0
   asm volatile(
       "{\n"
@@ -119,7 +119,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(su32(b)),
-      "r"(parity), "r"(20)
+      "r"(parity), "r"(hint)
       : "memory");
 #else
   asm volatile(
@@ -143,10 +143,11 @@ __device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
 // 7 converter arrive full_op
 constexpr int TL_N = 256;
 __device__ unsigned long long g_tctl[24][TL_N];
-__device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc) {
-  if (!on) { mbar_wait(b, parity); return; }
+__device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc,
+                                            uint32_t hint = 20) {
+  if (!on) { mbar_wait(b, parity, hint); return; }
   const unsigned long long t0 = clock64();
-  mbar_wait(b, parity);
+  mbar_wait(b, parity, hint);
   acc += clock64() - t0;
 }
 
@@ -381,6 +382,9 @@ struct MnDesc {
   // top 19 bits of a tf32 operand, i.e. trunc(x)), lo = rna_tf32(x - trunc(x)) beside it - one
   // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
   int btrunc = 1;
+  // mbarrier try_wait suspend-time hints (ns) of the producers / converters / epilogue waits: a
+  // spinning waiter takes issue slots from the working warps of its SM sub-partition
+  uint32_t hint_p = 20, hint_c = 20, hint_e = 20;
 };
 
 // Instruction descriptor for kind::tf32 with fp32 accumulation.
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(NT, 1)
         int b, mt, nt;
         tile_of(t, b, mt, nt);
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait_t(&a_empty[s], ph ^ 1, mn.prof, pacc[0]);
+          mbar_wait_t(&a_empty[s], ph ^ 1, mn.prof, pacc[0], mn.hint_p);
           uint8_t* sA = sAr + s * C_::A_BYTES;
           if (mn.dbg & 32) mbar_arrive(&a_full[s]);  // dev experiment: no A traffic
           else {
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(NT, 1)
         int b, mt, nt;
         tile_of(t, b, mt, nt);
         for (int kb = 0; kb < nk; ++kb, ++jq) {
-          mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0]);
+          mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0], mn.hint_p);
           if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
           uint8_t* sBl = sBh + C_::B_BYTES;
@@ -618,7 +622,7 @@ __global__ void __launch_bounds__(NT, 1)
       uint32_t jb = 0;
       for (int t = cid; t < total; t += ncl)
         for (int kb = 0; kb < nk; ++kb, ++jb) {
-          mbar_wait(&b_full[jb % SB], (jb / SB) & 1u);
+          mbar_wait(&b_full[jb % SB], (jb / SB) & 1u, mn.hint_p);
           mbar_arrive_cta(&b_full[jb % SB], 0);
         }
     }
@@ -634,7 +638,7 @@ __global__ void __launch_bounds__(NT, 1)
     for (int t = cid; t < total; t += ncl) {
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         // A first (the TMEM slot write is the long pole), then raw B planes if any
-        mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0]);
+        mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0], mn.hint_c);
         const bool tlc = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
         if (tlc) atomicMax(&g_tctl[6][jb], clock64());  // last converter warp has A
         const uint8_t* stA = sAr + sa * C_::A_BYTES;
@@ -672,7 +676,7 @@ __global__ void __launch_bounds__(NT, 1)
         const bool tc0 = tlc && warp == W_CONV0;  // converter warp 0 phase stamps
         if (tc0) g_tctl[8][jb] = clock64();
         const uint32_t as = jb % C_::NAS;
-        mbar_wait_t(&afree[as], ((jb / C_::NAS) & 1) ^ 1, mn.prof, pacc[1]);
+        mbar_wait_t(&afree[as], ((jb / C_::NAS) & 1) ^ 1, mn.prof, pacc[1], mn.hint_c);
         tc_fence_after();
         if (tc0) g_tctl[9][jb] = clock64();
         if (!(mn.dbg & 2)) {
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(NT, 1)
         if (tc0) g_tctl[10][jb] = clock64();
         if (!B_PRE && !ESPLIT) {  // B planes in shared memory: hi in place, lo beside it
           uint8_t* stB = sBr + sb * C_::B_STAGE;
-          mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2]);
+          mbar_wait_t(&b_full[sb], phb, mn.prof, pacc[2], mn.hint_c);
           if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0) atomicMax(&g_tctl[4][jb], clock64());
           if (tc0) g_tctl[11][jb] = clock64();
           float4* bh = (float4*)stB;
@@ -871,7 +875,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
       for (int kb = 0; kb < nk; ++kb, ++jb) {
         const uint32_t buf = jb % NACC;
-        mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0]);
+        mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0], mn.hint_e);
         const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
         const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
 
@@ -1153,6 +1157,9 @@ struct TcPlanner {
     if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
+    if (const char* f = getenv("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
+    if (const char* f = getenv("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
+    if (const char* f = getenv("HMC_TC_HINT_E")) mn.hint_e = (uint32_t)atoi(f);
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
