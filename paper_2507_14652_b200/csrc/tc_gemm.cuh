@@ -53,6 +53,9 @@ constexpr int NT = (4 + NCONV + NEPI) * 32;  // 512 threads
 constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TMA_A + 1, W_MMA = W_TMA_B + 1,
               W_MMA2 = W_MMA + 1;
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
+#ifndef TC_FOLD
+#define TC_FOLD 2  // K blocks per TMEM accumulator chunk (DESIGN.md §5 "accumulation")
+#endif
 
 // WG: the weight-gradient layout - no output staging (the epilogue writes the compacted k-vector
 // from registers), the freed shared memory deepens the B ring, whose raw planes the epilogue
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int SA = C_::SA, SB = C_::SB, NACC = C_::NACC, NC = C_::NC, NGRP = C_::NGRP;
   // raw B planes split by the epilogue warps (EPI_WGRAD), ESPLIT_D K blocks ahead of the fold
   constexpr bool ESPLIT = (EPI == EPI_WGRAD) && !B_PRE;
-  constexpr uint32_t ESPLIT_D = 2;
+  constexpr uint32_t ESPLIT_D = 2 * TC_FOLD;
   // EPI_DACT reads act'(dsrc) and EPI_RESID reads V tile by tile: TMA-loaded (mX) into the
   // staging buffers while the tile's K blocks are still in flight
   const bool loadx = (EPI == EPI_RESID) || (EPI == EPI_DACT && a.act != ACT_ID);
@@ -563,10 +566,11 @@ __global__ void __launch_bounds__(NT, 1)
     }
   } else if (warp == W_MMA || warp == W_MMA2) {
     // ================================ MMA issuer ==================================
-    // per K block, into the block's own accumulator (folded by the epilogue): the 8 small
-    // products Al.Bh + Ah.Bl first (truncated relative to a small partial sum), then the 4 big
-    // ones Ah.Bh.  The whole warp runs the loop (all values warp-uniform, so they live in uniform
-    // registers); one elected lane issues the MMAs and commits.
+    // per chunk of TC_FOLD K blocks, into the chunk's own accumulator (folded by the epilogue):
+    // the small products Al.Bh + Ah.Bl of all the chunk's blocks first (truncated relative to a
+    // small partial sum), then its big ones Ah.Bh (DESIGN.md §5 "accumulation").  The two issuers
+    // own alternate chunks.  The whole warp runs the loop (all values warp-uniform, so they live
+    // in uniform registers); one elected lane issues the MMAs and commits.
     if (crank == 0) {
       // leader: pair MMAs M = 256 (128 rows per CTA) x N = BN
       constexpr uint32_t IDESC = idesc_tf32(2 * BM, BN, 0, B_MN ? 1 : 0);
@@ -575,46 +579,57 @@ __global__ void __launch_bounds__(NT, 1)
       // by adding byte offsets >> 4 (all shared addresses < 256 KB)
       const uint64_t dB0 = sdesc(su32(sBr), b_lbo, b_sbo, b_lay);
       const uint32_t kstep16 = (B_MN ? mn.kstep : 32) >> 4;
-      const uint32_t mine = (warp == W_MMA2) ? 1u : 0u;  // K-block parity this issuer owns
-      uint32_t jb = 0;  // K blocks of this CTA so far (both issuers count all of them)
+      const uint32_t mine = (warp == W_MMA2) ? 1u : 0u;  // chunk parity this issuer owns
+      uint32_t jb = 0, jc = 0;  // K blocks / chunks of this CTA so far (both issuers count all)
       for (int t = cid; t < total; t += ncl) {
-        for (int kb = 0; kb < nk; ++kb, ++jb) {
-          if ((jb & 1u) != mine) continue;
-          const int s = (int)(jb % SB);
-          const uint32_t ph = (jb / SB) & 1u;
-          const uint32_t buf = jb % NACC;
-          const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
-
-          mbar_wait_cl_t(&tempty[buf], ((jb / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
-          if (tl) g_tctl[1][jb] = clock64();
-          tc_fence_after();
-          mbar_wait_cl_t(&full_op[jb % C_::NAS], (jb / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
-          if (B_PRE) mbar_wait_cl(&b_full[s], ph);  // (raw B planes are waited for by their splitters)
-          if (ESPLIT) mbar_wait_cl(&bsplit[s], ph);
-          if (tl) g_tctl[2][jb] = clock64();
+        for (int kb0 = 0; kb0 < nk; kb0 += TC_FOLD, ++jc) {
+          const int nkb = min(TC_FOLD, nk - kb0);
+          if ((jc & 1u) != mine) { jb += nkb; continue; }
+          const uint32_t buf = jc % NACC;
+          const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jc < TL_N && lane == 0;
+          mbar_wait_cl_t(&tempty[buf], ((jc / NACC) & 1) ^ 1, mn.prof && lane == 0, pacc[0]);
+          if (tl) g_tctl[1][jc] = clock64();
+          for (int i = 0; i < nkb; ++i) {
+            const uint32_t j = jb + i;
+            mbar_wait_cl_t(&full_op[j % C_::NAS], (j / C_::NAS) & 1, mn.prof && lane == 0, pacc[1]);
+            if (B_PRE) mbar_wait_cl(&b_full[j % SB], (j / SB) & 1u);  // (raw planes: waited for by their splitters)
+            if (ESPLIT) mbar_wait_cl(&bsplit[j % SB], (j / SB) & 1u);
+          }
+          if (tl) g_tctl[2][jc] = clock64();
           tc_fence_after();
           const uint32_t dcol = tmem_base + buf * BN;
-          const uint32_t aH = tmem_base + C_::A_COL0 + (jb % C_::NAS) * 64, aL = aH + 32;
-          const uint64_t dBh = dB0 + (uint64_t)((s * C_::B_STAGE) >> 4);
-          const uint64_t dBl = dBh + (uint64_t)(C_::B_BYTES >> 4);
           const unsigned long long t_i0 = mn.prof ? clock64() : 0ull;
           if (elect_one()) {
             if (!(mn.dbg & 1)) {
+              for (int i = 0; i < nkb; ++i) {
+                const uint32_t j = jb + i;
+                const uint32_t aH = tmem_base + C_::A_COL0 + (j % C_::NAS) * 64, aL = aH + 32;
+                const uint64_t dBh = dB0 + (uint64_t)(((j % SB) * C_::B_STAGE) >> 4);
+                const uint64_t dBl = dBh + (uint64_t)(C_::B_BYTES >> 4);
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              mma2_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, kk == 0 ? 0u : 1u);
-              mma2_tf32_ts(dcol, aH + 8 * kk, dBl + kk * kstep16, IDESC, 1u);
-            }
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                  mma2_tf32_ts(dcol, aL + 8 * kk, dBh + kk * kstep16, IDESC, (i == 0 && kk == 0) ? 0u : 1u);
+                  mma2_tf32_ts(dcol, aH + 8 * kk, dBl + kk * kstep16, IDESC, 1u);
+                }
+              }
+              for (int i = 0; i < nkb; ++i) {
+                const uint32_t j = jb + i;
+                const uint32_t aH = tmem_base + C_::A_COL0 + (j % C_::NAS) * 64;
+                const uint64_t dBh = dB0 + (uint64_t)(((j % SB) * C_::B_STAGE) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) mma2_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
+                for (int kk = 0; kk < BK / 8; ++kk) mma2_tf32_ts(dcol, aH + 8 * kk, dBh + kk * kstep16, IDESC, 1u);
+              }
             }
-            mma2_commit_mc(&b_empty[s]);
-            mma2_commit_mc(&afree[jb % C_::NAS]);
+            for (int i = 0; i < nkb; ++i) {
+              mma2_commit_mc(&b_empty[(jb + i) % SB]);
+              mma2_commit_mc(&afree[(jb + i) % C_::NAS]);
+            }
             mma2_commit_mc(&tfull[buf]);
           }
           __syncwarp();
+          jb += nkb;
           if (mn.prof) pacc[2] += clock64() - t_i0;
-          if (tl) g_tctl[3][jb] = clock64();
+          if (tl) g_tctl[3][jc] = clock64();
         }
       }
     } else if (B_PRE && warp == W_MMA && lane == 0) {
@@ -846,7 +861,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     };
     if (ESPLIT) split_upto(ESPLIT_D);
-    uint32_t jb = 0, jt = 0;
+    uint32_t jb = 0, jc = 0, jt = 0;
     for (int t = cid; t < total; t += ncl, ++jt) {
       int b, mt, nt;
       tile_of(t, b, mt, nt);
@@ -873,14 +888,14 @@ __global__ void __launch_bounds__(NT, 1)
           bias_l[u] = (bias && nb + col < a.N) ? __ldg(bias + col) : 0.f;
         }
       }
-      for (int kb = 0; kb < nk; ++kb, ++jb) {
-        const uint32_t buf = jb % NACC;
-        mbar_wait_t(&tfull[buf], (jb / NACC) & 1, mn.prof, pacc[0], mn.hint_e);
-        const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0 && ew == 0;
-        const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
-
-        const bool te = tl && blockIdx.x == 0;  // epilogue warp 0 phase stamps
-        if (te) g_tctl[16][jb] = clock64();
+      const int nch = (nk + TC_FOLD - 1) / TC_FOLD;
+      for (int c = 0; c < nch; ++c, ++jc) {
+        jb += min(TC_FOLD, nk - c * TC_FOLD);  // K blocks consumed through this chunk
+        const uint32_t buf = jc % NACC;
+        mbar_wait_t(&tfull[buf], (jc / NACC) & 1, mn.prof, pacc[0], mn.hint_e);
+        const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jc < TL_N && lane == 0;
+        const bool te = tla && ew == 0;  // epilogue warp 0 phase stamps (per chunk)
+        if (te) g_tctl[16][jc] = clock64();
         tc_fence_after();
         const uint32_t taddr = tmem_base + t_lane + buf * BN + half * NC;
 #pragma unroll
@@ -897,28 +912,33 @@ __global__ void __launch_bounds__(NT, 1)
                  acc[c0 + 16 + i], acc[c0 + 17 + i]);
           }
         }
-        if (te) g_tctl[17][jb] = clock64();
+        if (te) g_tctl[17][jc] = clock64();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(&tempty[buf], 0);
-        if (tla) atomicMax(&g_tctl[5][jb], clock64());  // last epilogue warp done
-        if (te) g_tctl[18][jb] = clock64();
-        if (ESPLIT) split_upto(jb + 1 + ESPLIT_D);
-        if (pend > 0) {  // one step of the parked tile per K block
+        if (tla) atomicMax(&g_tctl[5][jc], clock64());  // last epilogue warp done
+        if (te) g_tctl[18][jc] = clock64();
+        if (ESPLIT) split_upto(jb + ESPLIT_D);  // B stages of K blocks < jb + ESPLIT_D
+        if (pend > 0) {
+          // the parked tile's steps spread evenly over this tile's folds, the last one a fold
+          // before the tile end (its store's read of the staging tile is done by the next park)
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
-          tstep = te; tstep_j = jb;
-          emit_step(p_next++);
-          tstep = false;
-          if (--pend == 0 && loadx && !prefetched) {
-            staging_free();
-            issue_prefetch(b, mt, nt);
-            prefetched = true;
+          const int left = max(1, nch - 1 - c);
+          for (int todo = (pend + left - 1) / left; todo > 0 && pend > 0; --todo) {
+            tstep = te; tstep_j = jc;
+            emit_step(p_next++);
+            tstep = false;
+            if (--pend == 0 && loadx && !prefetched) {
+              staging_free();
+              issue_prefetch(b, mt, nt);
+              prefetched = true;
+            }
           }
           if (mn.prof) pacc[2] += clock64() - t_e0;
         }
-        if (te) g_tctl[19][jb] = clock64();
+        if (te) g_tctl[19][jc] = clock64();
       }
-      const bool tt = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb - 1 < TL_N && lane == 0 && ew == 0;
+      const bool tt = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jc - 1 < TL_N && lane == 0 && ew == 0;
       const unsigned long long t_out0 = mn.prof ? clock64() : 0ull;
       while (pend > 0) {  // short K: flush the parked tile
         emit_step(p_next++);
@@ -929,14 +949,14 @@ __global__ void __launch_bounds__(NT, 1)
         issue_prefetch(b, mt, nt);
       }
       if (!loadx) staging_free();
-      if (tt) g_tctl[20][jb - 1] = clock64();
+      if (tt) g_tctl[20][jc - 1] = clock64();
       if (EPI == EPI_FWD) {  // + bias (column u*32 + l lives in lane l's bias_l[u])
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] += __shfl_sync(0xffffffffu, bias_l[i >> 5], i & 31);
       }
       // ---- tile end: the register part of the fused epilogue, parked in staging ----
       if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
-      if (tt) g_tctl[21][jb - 1] = clock64();
+      if (tt) g_tctl[21][jc - 1] = clock64();
       const int m = mt * BM + 32 * quad + lane;
       const bool mrow = m < a.M;
       double psq = 0.0, pr = 0.0;
@@ -1036,7 +1056,7 @@ __global__ void __launch_bounds__(NT, 1)
         p_blk = mt * 4 + quad;
         __syncwarp();
       }
-      if (tt) g_tctl[22][jb - 1] = clock64();
+      if (tt) g_tctl[22][jc - 1] = clock64();
       if (mn.prof) pacc[2] += clock64() - t_out0;
       if (EPI == EPI_RESID) {
         // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps
