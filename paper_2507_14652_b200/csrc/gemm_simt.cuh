@@ -34,6 +34,10 @@ struct GemmArgs {
   const float* dsrc; int64_t ld_dsrc, s_dsrc;
   // EPI_WGRAD: slot_w[m*n_in + n] (n < n_in) or slot_b[m] (n == ones_col); -1 = frozen
   const int32_t* slot_w; const int32_t* slot_b; int n_in;
+  // optional compact form of slot_w for the tensor-core epilogue: per row m and 32-column group
+  // g, gmask[m*n_grp + g] = active columns, gbase[...] = slot of the group's first active entry
+  // (slots are ranks of ascending flat indices, so slot(m, 32g + j) = gbase + popc(mask below j))
+  const uint32_t* gmask; const int32_t* gbase; int n_grp;
   float* gl; int64_t k;
   // EPI_RESID: R = (V - (acc + b0)) * inv_s2; partial sums of r^2 and of R per tile (fp64)
   const float* V; int64_t ldv;

@@ -37,6 +37,7 @@ struct LayerInfo {
   bool tc_w = false;          // weights kept as tf32 hi/lo planes for the tensor-core engine
   bool bias_active = false;
   int64_t q_off = 0;           // offset of this layer's weights in the hi/lo planes
+  int64_t g_off = -1;          // offset of this layer's [n_out x ceil(n_in/32)] group masks (d_gmask)
   float* A = nullptr;  // [C x rows x n_out] layer output (hidden layers)
   float* D = nullptr;  // [C x rows x n_out] cos(z) for sin layers
 };
@@ -83,6 +84,8 @@ struct hmc_ctx {
   int64_t Ptc = 0;
   int colred_cap = 0;
   int32_t *d_idx = nullptr, *d_slot = nullptr;
+  uint32_t* d_gmask = nullptr;  // per-layer 32-column group masks of the slot map (tc WGRAD epilogue)
+  int32_t* d_gbase = nullptr;
   float* d_inv_mass = nullptr;
   uint32_t* d_chain = nullptr;
   float *cur_theta = nullptr, *cur_grad = nullptr, *wrk_theta = nullptr, *wrk_grad = nullptr, *p = nullptr;
@@ -376,6 +379,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.sq = x->sq;
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
+      if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
       const int id = prof_begin(x, st);
       bool tc = x->tc.accepts(a, false, false);
       if (tc) tc = x->tc.launch(a, false, false, st);
@@ -929,6 +933,32 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   const int C = x->C;
   x->d_idx = dalloc<int32_t>(x, x->k, err);
   x->d_slot = dalloc<int32_t>(x, x->P, err);
+  {  // group masks / bases of the slot map, for layers whose weights leave the tensor-core engine
+    std::vector<uint32_t> gm;
+    std::vector<int32_t> gb;
+    for (auto& L : x->layers) {
+      if (!L.any_active) continue;
+      const int G = (L.n_in + 31) / 32;
+      L.g_off = (int64_t)gm.size();
+      for (int m = 0; m < L.n_out; ++m)
+        for (int g = 0; g < G; ++g) {
+          uint32_t mk = 0;
+          int32_t base = -1;
+          for (int j = 0; j < 32 && 32 * g + j < L.n_in; ++j) {
+            const int32_t sl = slot[L.w_off + (int64_t)m * L.n_in + 32 * g + j];
+            if (sl >= 0) { mk |= 1u << j; if (base < 0) base = sl; }
+          }
+          gm.push_back(mk);
+          gb.push_back(base < 0 ? 0 : base);
+        }
+    }
+    x->d_gmask = dalloc<uint32_t>(x, gm.size(), err);
+    x->d_gbase = dalloc<int32_t>(x, gb.size(), err);
+    if (!gm.empty()) {
+      CK(cudaMemcpy(x->d_gmask, gm.data(), gm.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(x->d_gbase, gb.data(), gb.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
   x->d_chain = dalloc<uint32_t>(x, C, err);
   if (!h_im.empty()) x->d_inv_mass = dalloc<float>(x, x->k, err);
   x->Wd = dalloc<float>(x, (size_t)C * x->P, err);

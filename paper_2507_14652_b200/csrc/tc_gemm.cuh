@@ -385,6 +385,7 @@ struct MnDesc {
   // top 19 bits of a tf32 operand, i.e. trunc(x)), lo = rna_tf32(x - trunc(x)) beside it - one
   // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
   int btrunc = 1;
+  int tanh_end = 0;  // EPI_FWD tanh in registers at the tile end (1) or in emit steps (0): equal speed (measured)
   // mbarrier try_wait suspend-time hints (ns) of the producers / converters / epilogue waits: a
   // spinning waiter takes issue slots from the working warps of its SM sub-partition
   uint32_t hint_p = 20, hint_c = 20, hint_e = 20;
@@ -765,7 +766,10 @@ __global__ void __launch_bounds__(NT, 1)
     // 3 steps per 32-column group (12 / 12 / 8 columns of tanh, then the store), others 1 step;
     // with 8 K blocks per tile the last store is issued two folds before the tile end, so its
     // read of the staging tile has completed when the next tile is parked
-    const int nstep = (EPI == EPI_FWD && a.act == ACT_TANH) ? 3 : 1;
+    // tanh at the tile end in registers (mn.tanh_end: 64 independent elements per thread keep the
+    // MUFU pipe busy) or in 3 emit steps per group from the staging tile (12 / 12 / 8 columns)
+    const bool tanh_end = (EPI == EPI_FWD && a.act == ACT_TANH && mn.tanh_end);
+    const int nstep = (EPI == EPI_FWD && a.act == ACT_TANH && !tanh_end) ? 3 : 1;
     bool tstep = false;  // timeline: stamp the end of the emit step's register work (row 23)
     uint32_t tstep_j = 0;
     auto emit_step = [&](int k) {
@@ -774,16 +778,24 @@ __global__ void __launch_bounds__(NT, 1)
       uint8_t* stg = stg0 + g * STG;
       float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
       const int n0 = p_nb + 32 * g;
-      if (EPI == EPI_FWD && a.act == ACT_TANH) {
-#pragma unroll
-        for (int qq = 0; qq < 3; ++qq) {
-          const int q = 3 * part + qq;
-          if (q >= 8) break;
-          float4 z = srow[q ^ (lane & 7)];
-          tanh_acc2(z.x, z.y);
-          tanh_acc2(z.z, z.w);
-          srow[q ^ (lane & 7)] = z;
+      if (EPI == EPI_FWD && a.act == ACT_TANH && nstep == 3) {
+        // chunks 3 part .. 3 part + 2 (< 8) of the row: loads first (the stores would otherwise
+        // order each load after the previous chunk's store), six independent tanh pairs
+        const int q0 = 3 * part;
+        float4 z0 = srow[q0 ^ (lane & 7)];
+        float4 z1 = srow[(q0 + 1) ^ (lane & 7)];
+        float4 z2 = (q0 + 2 < 8) ? srow[(q0 + 2) ^ (lane & 7)] : z1;
+        tanh_acc2(z0.x, z0.y);
+        tanh_acc2(z0.z, z0.w);
+        tanh_acc2(z1.x, z1.y);
+        tanh_acc2(z1.z, z1.w);
+        if (q0 + 2 < 8) {  // (warp-uniform)
+          tanh_acc2(z2.x, z2.y);
+          tanh_acc2(z2.z, z2.w);
         }
+        srow[q0 ^ (lane & 7)] = z0;
+        srow[(q0 + 1) ^ (lane & 7)] = z1;
+        if (q0 + 2 < 8) srow[(q0 + 2) ^ (lane & 7)] = z2;
       }
       if (tstep) g_tctl[23][tstep_j] = clock64();
       if (part != nstep - 1) return;
@@ -879,6 +891,21 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < NC; ++i) acc[i] = 0.f;
       float bias_l[NC / 32];
+      // EPI_WGRAD with the compact slot map: this row's group masks / bases, loaded now and
+      // consumed at the tile end (the load latency hides behind the folds)
+      uint32_t gmk[NC / 32];
+      int32_t gbs[NC / 32];
+      if (EPI == EPI_WGRAD && a.gmask) {
+        const int m = mt * BM + 32 * quad + lane;
+#pragma unroll
+        for (int u = 0; u < NC / 32; ++u) {
+          const int n0 = nt * BN + half * NC + 32 * u;
+          const bool ok = m < a.M && n0 < a.N;
+          const int64_t gi = (int64_t)m * a.n_grp + (n0 >> 5);
+          gmk[u] = ok ? __ldg(a.gmask + gi) : 0u;
+          gbs[u] = ok ? __ldg(a.gbase + gi) : 0;
+        }
+      }
       {
         const int nb = nt * BN + half * NC;
         const float* bias = (EPI == EPI_FWD && a.bias) ? a.bias + (int64_t)b * a.s_bias + nb : nullptr;
@@ -953,6 +980,10 @@ __global__ void __launch_bounds__(NT, 1)
       if (EPI == EPI_FWD) {  // + bias (column u*32 + l lives in lane l's bias_l[u])
 #pragma unroll
         for (int i = 0; i < NC; ++i) acc[i] += __shfl_sync(0xffffffffu, bias_l[i >> 5], i & 31);
+        if (tanh_end) {
+#pragma unroll
+          for (int i = 0; i < NC; i += 2) tanh_acc2(acc[i], acc[i + 1]);
+        }
       }
       // ---- tile end: the register part of the fused epilogue, parked in staging ----
       if (loadx) mbar_wait_t(&xfull[ew], jt & 1, mn.prof, pacc[1]);
@@ -967,24 +998,36 @@ __global__ void __launch_bounds__(NT, 1)
         const int n0 = nt * BN + half * NC + 32 * g;
         float* v = acc + 32 * g;  // compile-time offsets after unrolling: stays in registers
         if (EPI == EPI_WGRAD) {
-          if (mrow && n0 < a.N) {
+          if (a.gmask) {  // compact slot map: one mask + one base per group (zero mask outside)
+            const uint32_t mk = gmk[g];
+            if (mk) {
+              float* gl = a.gl + (int64_t)b * a.k + gbs[g];
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((mk >> j) & 1u) gl[__popc(mk & ((1u << j) - 1u))] = v[j];
+            }
+          } else if (mrow && n0 < a.N) {
             const int32_t* sw = a.slot_w + (int64_t)m * a.n_in + n0;
             float* gl = a.gl + (int64_t)b * a.k;
             const bool full = vec_sl && n0 + 32 <= a.N;
+            // all 8 slot loads first (one round trip), then the scattered stores
+            int4 s4[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              int4 s4;
-              if (full) s4 = __ldg(reinterpret_cast<const int4*>(sw) + q);
+              if (full) s4[q] = __ldg(reinterpret_cast<const int4*>(sw) + q);
               else {
-                s4.x = (n0 + 4 * q + 0 < a.N) ? sw[4 * q + 0] : -1;
-                s4.y = (n0 + 4 * q + 1 < a.N) ? sw[4 * q + 1] : -1;
-                s4.z = (n0 + 4 * q + 2 < a.N) ? sw[4 * q + 2] : -1;
-                s4.w = (n0 + 4 * q + 3 < a.N) ? sw[4 * q + 3] : -1;
+                s4[q].x = (n0 + 4 * q + 0 < a.N) ? __ldg(sw + 4 * q + 0) : -1;
+                s4[q].y = (n0 + 4 * q + 1 < a.N) ? __ldg(sw + 4 * q + 1) : -1;
+                s4[q].z = (n0 + 4 * q + 2 < a.N) ? __ldg(sw + 4 * q + 2) : -1;
+                s4[q].w = (n0 + 4 * q + 3 < a.N) ? __ldg(sw + 4 * q + 3) : -1;
               }
-              if (s4.x >= 0) gl[s4.x] = v[4 * q];
-              if (s4.y >= 0) gl[s4.y] = v[4 * q + 1];
-              if (s4.z >= 0) gl[s4.z] = v[4 * q + 2];
-              if (s4.w >= 0) gl[s4.w] = v[4 * q + 3];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (s4[q].x >= 0) gl[s4[q].x] = v[4 * q];
+              if (s4[q].y >= 0) gl[s4[q].y] = v[4 * q + 1];
+              if (s4[q].z >= 0) gl[s4[q].z] = v[4 * q + 2];
+              if (s4[q].w >= 0) gl[s4[q].w] = v[4 * q + 3];
             }
           }
           continue;
@@ -1177,6 +1220,7 @@ struct TcPlanner {
     if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
+    if (const char* f = getenv("HMC_TC_TANHEND")) mn.tanh_end = atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_E")) mn.hint_e = (uint32_t)atoi(f);
