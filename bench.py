@@ -258,8 +258,12 @@ def run_ours(args):
                 traffic = json.load(open(tf)).get(args.cfg, {}).get(name)
             except Exception:
                 traffic = None
+        # traffic: ncu dram__bytes_read + dram__bytes_write of this class per launch (the json holds
+        # the class's bytes per evaluation, summed over its launches); algorithmic bytes beside it
+        traffic_pl = traffic / nl if (traffic is not None and nl) else None
         roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                    "frac": achieved / peak, "traffic": traffic, "kernel": name,
+                    "frac": achieved / peak, "traffic": traffic_pl, "traffic_unit": "bytes per launch",
+                    "algorithmic_bytes_per_launch": by / nl if nl else None, "kernel": name,
                     "launches_per_eval": nl, "ms_per_eval": ms,
                     "share_of_step0": ms / step0_total if step0_total else None,
                     "algorithmic_flops_per_eval": fl, "peak_source": peak_note}
