@@ -565,7 +565,8 @@ void enqueue_step(hmc_ctx* x, int mode, cudaStream_t st, std::string& err) {
   const int idf = prof_begin(x, st);
   if (mode == 1) {
     const int64_t total = (int64_t)x->C * x->k;
-    k_leapfrog<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(x->kstate());
+    (void)total;
+    k_leapfrog<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, st>>>(x->kstate());
   } else {
     k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), mode);
   }
@@ -700,7 +701,7 @@ void build_grad_graph(hmc_ctx* x, std::string& err) {
   const int64_t l0 = x->launches;
   x->prof_armed = false;
   try {
-    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
+    k_scatter<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
     x->launches++;
     enqueue_body(x, x->st);
     x->per_body = x->launches - l0 - 1;
@@ -1280,7 +1281,7 @@ int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, dou
       CK(cudaMemcpyAsync(x->wrk_theta + (size_t)c * x->k, dsamp + src * x->k, x->k * 4, cudaMemcpyDeviceToDevice,
                          x->st));
     }
-    k_scatter<<<148 * 4, 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
+    k_scatter<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
     (void)Ck;
     if (x->kind == HMC_MLP) {
       NetInfo& Nn = x->nets[0];

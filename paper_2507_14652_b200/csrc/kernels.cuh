@@ -64,12 +64,9 @@ __device__ __forceinline__ void put_param(const KState& s, int64_t c, int64_t j,
 
 // ---- scatter theta_s into the dense per-chain parameter vector (Theta_~s = mu_~s) --
 __global__ void k_scatter(KState s, const float* __restrict__ theta) {
-  const int64_t total = (int64_t)s.C * s.k;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / s.k, j = t - c * s.k;
-    put_param(s, c, j, theta[t]);
-  }
+  const int64_t c = blockIdx.y;  // chain (grid.y), entries j grid-strided over grid.x
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < s.k; j += (int64_t)gridDim.x * blockDim.x)
+    put_param(s, c, j, theta[c * s.k + j]);
 }
 
 // tf32 hi/lo planes of one layer's weights for every chain, from the dense parameters
@@ -213,7 +210,31 @@ __global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X,
     const float bias = (b_off >= 0) ? Wd[(int64_t)c * P + b_off + n] : 0.f;
     float* out = A + ((int64_t)c * rows + r0) * n_out + n;
     float* dout = D ? D + ((int64_t)c * rows + r0) * n_out + n : nullptr;
-    for (int r = 0; r < nr; ++r) {
+    int r = 0;
+    // 4 rows at a time: independent tanh chains (packed pairs, bitwise equal to tanh_acc)
+    for (; r + 4 <= nr; r += 4) {
+      float z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        z[u] = bias;
+#pragma unroll
+        for (int i = 0; i < DIN; ++i) z[u] = fmaf(xs[(r + u) * DIN + i], w[i], z[u]);
+      }
+      if (dout) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dout[(int64_t)(r + u) * n_out] = cosf(z[u]);
+      }
+      if (act == ACT_TANH) {
+        tanh_acc2(z[0], z[1]);
+        tanh_acc2(z[2], z[3]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) z[u] = act_fwd(act, z[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out[(int64_t)(r + u) * n_out] = z[u];
+    }
+    for (; r < nr; ++r) {
       float z = bias;
 #pragma unroll
       for (int i = 0; i < DIN; ++i) z = fmaf(xs[r * DIN + i], w[i], z);
@@ -241,7 +262,8 @@ __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict
 #pragma unroll
     for (int i = 0; i <= DIN; ++i) acc[i] = 0.f;
     const float* g = G + (int64_t)c * sG + r0 * n_out + o;
-    for (int r = 0; r < nr; ++r) {
+#pragma unroll 8
+    for (int r = 0; r < nr; ++r) {  // (unrolled: 8 loads of G in flight per thread)
       float gv = g[(int64_t)r * n_out];
       if (sq) gv *= gv;   // sensitivity mode: sum G^2 X^2 and sum G^2
 #pragma unroll
@@ -423,7 +445,8 @@ __global__ void k_colsum_reduce(const float* __restrict__ colsum, int64_t s_cols
     if (sl < 0) continue;
     const float* p = colsum + (int64_t)c * s_colsum + o;
     float acc = 0.f;
-    for (int blk = 0; blk < nblk; ++blk) acc += p[(int64_t)blk * N];
+#pragma unroll 8
+    for (int blk = 0; blk < nblk; ++blk) acc += p[(int64_t)blk * N];  // (8 loads in flight, same order)
     gl[(int64_t)c * k + sl] = acc;
   }
 }
@@ -484,11 +507,10 @@ __global__ void __launch_bounds__(KT) k_finalize(KState s, int mode) {
 //      full kick p += eps g, drift theta += eps M^-1 p, scatter.  log pi is not needed at the
 //      inner points (only at the trajectory end, k_finalize mode 2), so no reduction here ----
 __global__ void __launch_bounds__(256) k_leapfrog(KState s) {
-  const int64_t total = (int64_t)s.C * s.k;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / s.k, j = t - c * s.k;
-    const float fe = (float)s.eps[c];
+  const int64_t c = blockIdx.y;  // chain (grid.y), entries j grid-strided over grid.x
+  const float fe = (float)s.eps[c];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < s.k; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = c * s.k + j;
     float th = s.wrk_theta[t];
     const float g = s.gl[t] - (float)((double)th * s.inv_sp2);
     s.wrk_grad[t] = g;
