@@ -38,6 +38,9 @@ struct GemmArgs {
   // g, gmask[m*n_grp + g] = active columns, gbase[...] = slot of the group's first active entry
   // (slots are ranks of ascending flat indices, so slot(m, 32g + j) = gbase + popc(mask below j))
   const uint32_t* gmask; const int32_t* gbase; int n_grp;
+  // tensor-core EPI_WGRAD split over K (ksplit > 1): split s writes its partial k-vector entries
+  // to gl_part + s * batch * k (summed in fixed order afterwards)
+  int ksplit; float* gl_part;
   float* gl; int64_t k;
   // EPI_RESID: R = (V - (acc + b0)) * inv_s2; partial sums of r^2 and of R per tile (fp64)
   const float* V; int64_t ldv;

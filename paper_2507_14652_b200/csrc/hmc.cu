@@ -38,6 +38,8 @@ struct LayerInfo {
   bool bias_active = false;
   int64_t q_off = 0;           // offset of this layer's weights in the hi/lo planes
   int64_t g_off = -1;          // offset of this layer's [n_out x ceil(n_in/32)] group masks (d_gmask)
+  int64_t ws_lo = 0, ws_hi = 0; // k-slot range of this layer's active weights
+  int ksplit = 1;               // K split of its tensor-core weight-gradient GEMM
   float* A = nullptr;  // [C x rows x n_out] layer output (hidden layers)
   float* D = nullptr;  // [C x rows x n_out] cos(z) for sin layers
 };
@@ -86,6 +88,7 @@ struct hmc_ctx {
   int32_t *d_idx = nullptr, *d_slot = nullptr;
   uint32_t* d_gmask = nullptr;  // per-layer 32-column group masks of the slot map (tc WGRAD epilogue)
   int32_t* d_gbase = nullptr;
+  float* gl_part = nullptr;     // [ksplit_max x C x k] K-split weight-gradient partials
   float* d_inv_mass = nullptr;
   uint32_t* d_chain = nullptr;
   float *cur_theta = nullptr, *cur_grad = nullptr, *wrk_theta = nullptr, *wrk_grad = nullptr, *p = nullptr;
@@ -380,11 +383,17 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
+      if (L.ksplit > 1 && x->gl_part) { a.ksplit = L.ksplit; a.gl_part = x->gl_part; }
       const int id = prof_begin(x, st);
       bool tc = x->tc.accepts(a, false, false);
       if (tc) tc = x->tc.launch(a, false, false, st);
       if (tc) {
         x->launches++;
+        if (a.ksplit > 1) {  // fixed-order sum of the splits' partial k-vector entries
+          k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.ws_hi - L.ws_lo + 255) / 256, 256)), x->C),
+                            256, 0, st>>>(x->gl_part, a.ksplit, (int64_t)x->C * x->k, x->k, L.ws_lo, L.ws_hi, x->gl);
+          x->launches++;
+        }
         x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
         prof_end(x, id, st, "tc_wgrad", 2.0 * a.M * a.N * (double)a.K * a.batch,
                  4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
@@ -392,8 +401,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           const int id2 = prof_begin(x, st);
           if (N.cs_ready) {  // partials from the producing GEMM's epilogue
             const int nblk = (int)((L.rows + 31) / 32);
-            k_colsum_reduce<<<x->C, 256, 0, st>>>(N.colsum, (int64_t)nblk * L.n_out, nblk, L.n_out,
-                                                  x->d_slot + L.b_off, x->gl, x->k);
+            k_colsum_reduce<<<dim3((unsigned)((L.n_out + 31) / 32), x->C), 1024, 0, st>>>(
+                N.colsum, (int64_t)nblk * L.n_out, nblk, L.n_out, x->d_slot + L.b_off, x->gl, x->k);
             x->launches += 1;
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
@@ -953,6 +962,35 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
           gb.push_back(base < 0 ? 0 : base);
         }
     }
+    // slot ranges, and the K split of weight-gradient GEMMs with fewer CTA-pair tiles than the
+    // GPU has SM pairs (each split >= 8 K blocks of 32 rows)
+    int ks_max = 1;
+    for (auto& L : x->layers) {
+      L.ws_lo = L.ws_hi = 0;
+      bool first = true;
+      for (int64_t t = L.w_off; t < L.w_off + (int64_t)L.n_in * L.n_out; ++t)
+        if (slot[t] >= 0) {
+          if (first) { L.ws_lo = slot[t]; first = false; }
+          L.ws_hi = slot[t] + 1;
+        }
+      L.ksplit = 1;
+      if (x->tc.enabled && L.any_active && L.n_in > 8) {
+        const int64_t rows = x->nets[L.net].rows;  // (L.rows is filled in later)
+        GemmArgs pa = gemm_base(L.n_out, L.n_in, (int)rows, x->C);
+        const int pt = TcPlanner::pair_tiles(pa);
+        const int half_sms = std::max(1, x->tc.num_sms / 2);
+        const int nk = (int)((rows + 31) / 32);
+        if (pt < half_sms && nk >= 16) {  // fewest rounds of SM pairs per unit of K work
+          double best = 1.0;
+          for (int ks = 2; ks <= std::min(16, nk / 8); ++ks) {
+            const double cost = (double)((pt * ks + half_sms - 1) / half_sms) / ks;
+            if (cost < best - 1e-12) { best = cost; L.ksplit = ks; }
+          }
+        }
+        ks_max = std::max(ks_max, L.ksplit);
+      }
+    }
+    if (ks_max > 1) x->gl_part = dalloc<float>(x, (size_t)ks_max * x->C * x->k, err);
     x->d_gmask = dalloc<uint32_t>(x, gm.size(), err);
     x->d_gbase = dalloc<int32_t>(x, gb.size(), err);
     if (!gm.empty()) {

@@ -437,17 +437,45 @@ __global__ void k_sens_finalize(const float* __restrict__ sumsq, int C, int64_t 
 
 // ---- bias gradient from the column partials the tensor-core input-gradient epilogue wrote
 //      (one per 32-row block): gl[c][slot_b[o]] = sum_blk colsum[c][blk][o], fixed order ----
-__global__ void k_colsum_reduce(const float* __restrict__ colsum, int64_t s_colsum, int nblk, int N,
-                                const int32_t* __restrict__ slot_b, float* __restrict__ gl, int64_t k) {
-  const int c = blockIdx.x;
-  for (int o = threadIdx.x; o < N; o += blockDim.x) {
-    const int sl = slot_b[o];
-    if (sl < 0) continue;
+// bias gradient from the fused column partials: block (32-column group, chain) of 32 warps, warp w
+// sums row blocks w, w + 32, ... of its lane's column (coalesced 128 B rows), then the 32 warp sums
+// are added in warp order (fixed order: deterministic)
+__global__ void __launch_bounds__(1024) k_colsum_reduce(const float* __restrict__ colsum, int64_t s_colsum, int nblk,
+                                                       int N, const int32_t* __restrict__ slot_b,
+                                                       float* __restrict__ gl, int64_t k) {
+  __shared__ float part[32][33];
+  const int c = blockIdx.y;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int o = blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (o < N) {
     const float* p = colsum + (int64_t)c * s_colsum + o;
+#pragma unroll 4
+    for (int blk = w; blk < nblk; blk += 32) acc += p[(int64_t)blk * N];
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && o < N) {
+    const int sl = slot_b[o];
+    if (sl >= 0) {
+      float t = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) t += part[i][lane];
+      gl[(int64_t)c * k + sl] = t;
+    }
+  }
+}
+
+
+// ---- K-split weight gradient: gl[c][j] = sum_s part[s][c][j] in split order, j in this layer's
+//      weight-slot range [lo, hi) ----
+__global__ void k_ksplit_reduce(const float* __restrict__ part, int ksplit, int64_t Ck, int64_t k, int64_t lo,
+                                int64_t hi, float* __restrict__ gl) {
+  const int64_t c = blockIdx.y;
+  for (int64_t j = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < hi; j += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
-#pragma unroll 8
-    for (int blk = 0; blk < nblk; ++blk) acc += p[(int64_t)blk * N];  // (8 loads in flight, same order)
-    gl[(int64_t)c * k + sl] = acc;
+    for (int s = 0; s < ksplit; ++s) acc += part[(int64_t)s * Ck + c * k + j];
+    gl[c * k + j] = acc;
   }
 }
 

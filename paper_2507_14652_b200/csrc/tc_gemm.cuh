@@ -465,15 +465,25 @@ __global__ void __launch_bounds__(NT, 1)
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int n_mp = (n_mt + 1) >> 1;
   const int pairs_per_b = n_mp * n_nt;
-  const int total = pairs_per_b * a.batch;  // pair tiles
+  // EPI_WGRAD may split K (a.ksplit > 1, few output tiles): work item t = (pair tile, K split ks),
+  // the split's K blocks [kbeg, kend)
+  const int nk = (a.K + BK - 1) / BK;
+  const int ksplit = (EPI == EPI_WGRAD && a.ksplit > 1) ? a.ksplit : 1;
+  const int kper = (nk + ksplit - 1) / ksplit;
+  const int total = pairs_per_b * a.batch * ksplit;  // work items
   auto tile_of = [&](int t, int& b, int& mt, int& nt) {
+    t /= ksplit;
     b = t / pairs_per_b;
     const int rem = t - b * pairs_per_b;
     const int mp = rem / n_nt;
     nt = rem - mp * n_nt;
     mt = 2 * mp + (int)crank;
   };
-  const int nk = (a.K + BK - 1) / BK;
+  auto krange = [&](int t, int& kbeg, int& kend) {
+    const int ks = t % ksplit;
+    kbeg = ks * kper;
+    kend = min(nk, kbeg + kper);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
@@ -518,16 +528,21 @@ __global__ void __launch_bounds__(NT, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = cid; t < total; t += ncl) {
-        int b, mt, nt;
+        int b, mt, nt, kbeg, kend;
         tile_of(t, b, mt, nt);
-        for (int kb = 0; kb < nk; ++kb) {
+        krange(t, kbeg, kend);
+        for (int kb = kbeg; kb < kend; ++kb) {
           mbar_wait_t(&a_empty[s], ph ^ 1, mn.prof, pacc[0], mn.hint_p);
           uint8_t* sA = sAr + s * C_::A_BYTES;
           if (mn.dbg & 32) mbar_arrive(&a_full[s]);  // dev experiment: no A traffic
           else {
           mbar_expect_tx(&a_full[s], C_::A_BYTES);
-          if (A_MN) tma_load4(sA, &mA, &a_full[s], 0, kb * BK, mt * (BM / 32), b);
-          else tma_load3(sA, &mA, &a_full[s], kb * BK, mt * BM, b);
+          if (A_MN) {  // four 32-row blocks [m/32][k][m%32] (rows >= M zero-filled by the map)
+#pragma unroll
+            for (int i = 0; i < BM / 32; ++i)
+              tma_load3(sA + i * 4096, &mA, &a_full[s], mt * BM + 32 * i, kb * BK, a.sA ? b : 0);
+          }
+          else tma_load3(sA, &mA, &a_full[s], kb * BK, mt * BM, a.sA ? b : 0);
           }
           if (++s == SA) { s = 0; ph ^= 1; }
         }
@@ -541,9 +556,10 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t bytes = (B_PRE ? 2 : 1) * C_::B_BYTES;
       uint32_t jq = 0;
       for (int t = cid; t < total; t += ncl) {
-        int b, mt, nt;
+        int b, mt, nt, kbeg, kend;
         tile_of(t, b, mt, nt);
-        for (int kb = 0; kb < nk; ++kb, ++jq) {
+        krange(t, kbeg, kend);
+        for (int kb = kbeg; kb < kend; ++kb, ++jq) {
           mbar_wait_t(&b_empty[s], ph ^ 1, mn.prof, pacc[0], mn.hint_p);
           if (mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jq < TL_N) g_tctl[0][jq] = clock64();
           uint8_t* sBh = sBr + s * C_::B_STAGE;
@@ -554,10 +570,17 @@ __global__ void __launch_bounds__(NT, 1)
           else {
           mbar_expect_tx(&b_full[s], bytes);
           const int n_half = nt * BN + (int)crank * (BN / 2);
-          if (B_MN) tma_load4(sBh, &mB, &b_full[s], 0, kb * BK, n_half / 32, b);
-          else tma_load3(sBh, &mB, &b_full[s], kb * BK, n_half, b);
+          if (B_MN) {  // this CTA's two 32-column blocks (columns >= N zero-filled)
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load3(sBh + i * 4096, &mB, &b_full[s], n_half + 32 * i, kb * BK, (B_PRE || a.sB) ? b : 0);
+          }
+          else tma_load3(sBh, &mB, &b_full[s], kb * BK, n_half, (B_PRE || a.sB) ? b : 0);
           if (B_PRE) {
-            if (B_MN) tma_load4(sBl, &mB2, &b_full[s], 0, kb * BK, n_half / 32, b);
+            if (B_MN) {
+#pragma unroll
+              for (int i = 0; i < BN / 64; ++i) tma_load3(sBl + i * 4096, &mB2, &b_full[s], n_half + 32 * i, kb * BK, b);
+            }
             else tma_load3(sBl, &mB2, &b_full[s], kb * BK, n_half, b);
           }
           }
@@ -583,8 +606,10 @@ __global__ void __launch_bounds__(NT, 1)
       const uint32_t mine = (warp == W_MMA2) ? 1u : 0u;  // chunk parity this issuer owns
       uint32_t jb = 0, jc = 0;  // K blocks / chunks of this CTA so far (both issuers count all)
       for (int t = cid; t < total; t += ncl) {
-        for (int kb0 = 0; kb0 < nk; kb0 += TC_FOLD, ++jc) {
-          const int nkb = min(TC_FOLD, nk - kb0);
+        int kbeg, kend;
+        krange(t, kbeg, kend);
+        for (int kb0 = kbeg; kb0 < kend; kb0 += TC_FOLD, ++jc) {
+          const int nkb = min(TC_FOLD, kend - kb0);
           if ((jc & 1u) != mine) { jb += nkb; continue; }
           const uint32_t buf = jc % NACC;
           const bool tl = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jc < TL_N && lane == 0;
@@ -636,11 +661,14 @@ __global__ void __launch_bounds__(NT, 1)
     } else if (B_PRE && warp == W_MMA && lane == 0) {
       // peer: relay "my half of the pre-split B stage landed" to the leader's b_full
       uint32_t jb = 0;
-      for (int t = cid; t < total; t += ncl)
-        for (int kb = 0; kb < nk; ++kb, ++jb) {
+      for (int t = cid; t < total; t += ncl) {
+        int kbeg, kend;
+        krange(t, kbeg, kend);
+        for (int kb = kbeg; kb < kend; ++kb, ++jb) {
           mbar_wait(&b_full[jb % SB], (jb / SB) & 1u, mn.hint_p);
           mbar_arrive_cta(&b_full[jb % SB], 0);
         }
+      }
     }
   } else if (warp >= W_CONV0) {
     // ================================ converters ==================================
@@ -652,7 +680,9 @@ __global__ void __launch_bounds__(NT, 1)
     uint32_t pha = 0, phb = 0;
     uint32_t jb = 0;
     for (int t = cid; t < total; t += ncl) {
-      for (int kb = 0; kb < nk; ++kb, ++jb) {
+      int kbeg, kend;
+      krange(t, kbeg, kend);
+      for (int kb = kbeg; kb < kend; ++kb, ++jb) {
         // A first (the TMEM slot write is the long pole), then raw B planes if any
         mbar_wait_t(&a_full[sa], pha, mn.prof, pacc[0], mn.hint_c);
         const bool tlc = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jb < TL_N && lane == 0;
@@ -842,7 +872,12 @@ __global__ void __launch_bounds__(NT, 1)
     };
     // ESPLIT: raw B stages of this CTA's K blocks [js, lim) split in place (hi) and beside (lo),
     // each warp one eighth of the stage
-    const uint32_t my_kb = (cid < total) ? (uint32_t)((total - cid + ncl - 1) / ncl) * (uint32_t)nk : 0u;
+    uint32_t my_kb = 0;
+    for (int t = cid; t < total; t += ncl) {
+      int kbeg, kend;
+      krange(t, kbeg, kend);
+      my_kb += (uint32_t)(kend - kbeg);
+    }
     uint32_t js = 0;
     auto split_upto = [&](uint32_t lim) {
       for (; js < lim && js < my_kb; ++js) {
@@ -915,9 +950,12 @@ __global__ void __launch_bounds__(NT, 1)
           bias_l[u] = (bias && nb + col < a.N) ? __ldg(bias + col) : 0.f;
         }
       }
-      const int nch = (nk + TC_FOLD - 1) / TC_FOLD;
+      int kbeg, kend;
+      krange(t, kbeg, kend);
+      const int nkt = kend - kbeg;
+      const int nch = (nkt + TC_FOLD - 1) / TC_FOLD;
       for (int c = 0; c < nch; ++c, ++jc) {
-        jb += min(TC_FOLD, nk - c * TC_FOLD);  // K blocks consumed through this chunk
+        jb += min(TC_FOLD, nkt - c * TC_FOLD);  // K blocks consumed through this chunk
         const uint32_t buf = jc % NACC;
         mbar_wait_t(&tfull[buf], (jc / NACC) & 1, mn.prof, pacc[0], mn.hint_e);
         const bool tla = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && jc < TL_N && lane == 0;
@@ -1001,14 +1039,14 @@ __global__ void __launch_bounds__(NT, 1)
           if (a.gmask) {  // compact slot map: one mask + one base per group (zero mask outside)
             const uint32_t mk = gmk[g];
             if (mk) {
-              float* gl = a.gl + (int64_t)b * a.k + gbs[g];
+              float* gl = (ksplit > 1 ? a.gl_part + (int64_t)(t % ksplit) * a.batch * a.k : a.gl) + (int64_t)b * a.k + gbs[g];
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if ((mk >> j) & 1u) gl[__popc(mk & ((1u << j) - 1u))] = v[j];
             }
           } else if (mrow && n0 < a.N) {
             const int32_t* sw = a.slot_w + (int64_t)m * a.n_in + n0;
-            float* gl = a.gl + (int64_t)b * a.k;
+            float* gl = (ksplit > 1 ? a.gl_part + (int64_t)(t % ksplit) * a.batch * a.k : a.gl) + (int64_t)b * a.k;
             const bool full = vec_sl && n0 + 32 <= a.N;
             // all 8 slot loads first (one round trip), then the scattered stores
             int4 s4[8];
@@ -1259,14 +1297,14 @@ struct TcPlanner {
     }
     if (!find(amn, bmn, pre != nullptr, a.epi)) return false;
     if (a.epi == EPI_FWD && a.act == ACT_SIN) return false;
-    if ((a.lda % 4) || (a.sA % 4) || !al16(a.A) || (a.sA == 0 && a.batch > 1)) return false;
-    if (amn && (a.M % 32)) return false;
+    if ((a.lda % 4) || (a.sA % 4) || !al16(a.A)) return false;
+
     if (pre) {
       if (!pre->hi || (pre->ld % 4) || (pre->stride % 4) || !al16(pre->hi) || !al16(pre->lo)) return false;
     } else {
-      if ((a.ldb % 4) || (a.sB % 4) || !al16(a.B) || (a.sB == 0 && a.batch > 1)) return false;
+      if ((a.ldb % 4) || (a.sB % 4) || !al16(a.B)) return false;
     }
-    if (bmn && (a.N % 32)) return false;
+
     if (a.epi != EPI_WGRAD) {  // TMA store of the output
       if (!a.C || (a.ldc % 4) || (a.sC % 4) || !al16(a.C)) return false;
     }
@@ -1275,6 +1313,11 @@ struct TcPlanner {
     }
     if (a.epi == EPI_RESID && (!a.V || (a.ldv % 4) || !al16(a.V))) return false;
     return true;
+  }
+
+  // work items (CTA-pair tiles) of a launch without K split
+  static int pair_tiles(const GemmArgs& a) {
+    return (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch;
   }
 
   int n_tiles(const GemmArgs& a, bool akm, bool bkm) const {
@@ -1295,15 +1338,17 @@ struct TcPlanner {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
-  // MN-major operand X(k, j) = X[k*ld + j] per batch: dims (32, K, MN/32, batch), box (32, 32, box_mn/32, 1)
-  // (plain = no swizzle: the raw A tile only the converter warps read, [j/32][k][j%32])
+  // MN-major operand X(k, j) = X[k*ld + j] per batch: dims (MN, K, batch), box (32, 32, 1) - one
+  // 32-wide MN block of 32 K rows per load, [j/32][k][j%32] in shared memory; MN need not be a
+  // multiple of 32 (columns >= MN are zero-filled).  plain = no swizzle (the raw A tile only the
+  // converter warps read); otherwise the MMA's SWIZZLE_128B_BASE32B layout.
   bool map_mnmajor(CUtensorMap* m, const float* base, int64_t K, int64_t MN, int64_t ld, int64_t bstride,
-                   int batch, int box_mn, bool plain = false) const {
-    cuuint64_t dims[4] = {32, (cuuint64_t)K, (cuuint64_t)(MN / 32), (cuuint64_t)batch};
-    cuuint64_t strides[3] = {(cuuint64_t)ld * 4, 128, (cuuint64_t)(bstride ? bstride : K * ld) * 4};
-    cuuint32_t box[4] = {32, 32, (cuuint32_t)(box_mn / 32), 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
+                   int batch, int /*box_mn*/, bool plain = false) const {
+    cuuint64_t dims[3] = {(cuuint64_t)MN, (cuuint64_t)K, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)(bstride ? bstride : K * ld) * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, plain ? CU_TENSOR_MAP_SWIZZLE_NONE : mn_swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -1333,16 +1378,19 @@ struct TcPlanner {
     memset(&mB2, 0, sizeof(mB2));
     memset(&mC, 0, sizeof(mC));
     memset(&mX, 0, sizeof(mX));
-    bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, a.batch, tc::BM, true)
-                  : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, a.batch, tc::BM);
+    // an operand shared by every batch entry (stride 0, e.g. the data) is mapped once and loaded
+    // at batch coordinate 0 (the kernel reads a.sA / a.sB)
+    const int batA = a.sA == 0 ? 1 : a.batch, batB = a.sB == 0 ? 1 : a.batch;
+    bool ok = amn ? map_mnmajor(&mA, a.A, a.K, a.M, a.lda, a.sA, batA, tc::BM, true)
+                  : map_kmajor(&mA, a.A, a.M, a.K, a.lda, a.sA, batA, tc::BM);
     if (pre) {
       ok = ok && (bmn ? map_mnmajor(&mB, pre->hi, a.K, a.N, pre->ld, pre->stride, a.batch, BN / 2)
                       : map_kmajor(&mB, pre->hi, a.N, a.K, pre->ld, pre->stride, a.batch, BN / 2));
       ok = ok && (bmn ? map_mnmajor(&mB2, pre->lo, a.K, a.N, pre->ld, pre->stride, a.batch, BN / 2)
                       : map_kmajor(&mB2, pre->lo, a.N, a.K, pre->ld, pre->stride, a.batch, BN / 2));
     } else {  // (each CTA of the pair loads half of the B tile)
-      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, a.batch, BN / 2)
-                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, a.batch, BN / 2));
+      ok = ok && (bmn ? map_mnmajor(&mB, a.B, a.K, a.N, a.ldb, a.sB, batB, BN / 2)
+                      : map_kmajor(&mB, a.B, a.N, a.K, a.ldb, a.sB, batB, BN / 2));
       mB2 = mB;
     }
     if (a.epi != EPI_WGRAD) ok = ok && map_store(&mC, a.C, a.M, a.N, a.ldc, a.sC, a.batch);
@@ -1350,7 +1398,8 @@ struct TcPlanner {
       ok = ok && map_store(&mX, const_cast<float*>(a.dsrc), a.M, a.N, a.ld_dsrc, a.s_dsrc, a.batch);
     if (a.epi == EPI_RESID) ok = ok && map_store(&mX, const_cast<float*>(a.V), a.M, a.N, a.ldv, 0, 1);
     if (!ok) return false;
-    const int pairs = (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch;
+    const int pairs = (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch *
+                      ((a.epi == EPI_WGRAD && a.ksplit > 1) ? a.ksplit : 1);
     const int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
     int nv = 0;
     tc::MnDesc md = mn;
