@@ -385,6 +385,7 @@ struct MnDesc {
   // top 19 bits of a tf32 operand, i.e. trunc(x)), lo = rna_tf32(x - trunc(x)) beside it - one
   // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
   int btrunc = 1;
+  int pdl = 1;       // programmatic dependent launch (HMC_TC_PDL=0 disables)
   int tanh_end = 0;  // EPI_FWD tanh in registers at the tile end (1) or in emit steps (0): equal speed (measured)
   // mbarrier try_wait suspend-time hints (ns) of the producers / converters / epilogue waits: a
   // spinning waiter takes issue slots from the working warps of its SM sub-partition
@@ -518,6 +519,11 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
   tc_fence_after();
+  // programmatic dependent launch: everything above (barrier init, TMEM allocation, tensor-map
+  // prefetch) overlaps the previous kernel's tail; global memory is touched only after it has
+  // completed.  The next kernel may be launched now (its CTAs get an SM as ours exit).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
   unsigned long long pacc[3] = {0ull, 0ull, 0ull};
   const unsigned long long t_k0 = mn.prof ? clock64() : 0ull;
@@ -1259,6 +1265,7 @@ struct TcPlanner {
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
     if (const char* f = getenv("HMC_TC_TANHEND")) mn.tanh_end = atoi(f);
+    if (const char* f = getenv("HMC_TC_PDL")) mn.pdl = atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_E")) mn.hint_e = (uint32_t)atoi(f);
@@ -1410,13 +1417,15 @@ struct TcPlanner {
     cfg.blockDim = dim3(tc::NT);
     cfg.dynamicSmemBytes = v->smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see griddepcontrol in the kernel
+    attr[1].val.programmaticStreamSerializationAllowed = mn.pdl ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (cudaLaunchKernelEx(&cfg, v->fn, mA, mB, mB2, mC, mX, a, md) != cudaSuccess) return false;
     return true;
   }
