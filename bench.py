@@ -76,7 +76,7 @@ class Clocks:
         self.f.flush()
         rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()]
         os.unlink(self.f.name)
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             r = [x.strip() for x in r]
@@ -85,13 +85,17 @@ class Clocks:
                 mx.append(float(r[2]))
             except Exception:
                 continue
+            try:
+                pw.append(float(r[3]))
+            except Exception:
+                pass
             for nm, v in zip(names, r[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_min_mhz": min(sm), "sm_max_mhz": max(mx),
+                "power_w": statistics.median(pw) if pw else None, "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ------------------------------------------------------------------------- CPU oracle ---
@@ -283,10 +287,12 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        clk_e = Clocks(gpu_index)
         t0 = time.perf_counter()
         for s in range(Ke):
             abi.hmc_sample(ctx.ctx, hT, hLP, hG, eps, L, it + s, 1, hS, hA, hD)
         te = time.perf_counter() - t0
+        clocks_e2e = clk_e.stop()
         if world > 1:
             tt = torch.tensor([te], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -294,7 +300,7 @@ def run_ours(args):
         h2d = C * k * 4 * 2 + C * 8
         d2h = h2d + C * k * 4 + C + C * 8
         e2e = {"value": world * C * L * Ke / te, "unit": "evals/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": Ke}
+               "d2h_bytes_per_step": d2h, "steps": Ke, "clocks": clocks_e2e}
 
     per_grad, base, per_step = abi.hmc_launch_counts(ctx.ctx)
     launches = K * (base + L * per_step)
