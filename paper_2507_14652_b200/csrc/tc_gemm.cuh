@@ -62,8 +62,20 @@ constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32
 // warps split (they are idle between folds there; the converters keep A only)
 template <int BN, bool WG = false>
 struct Cfg {
-  static constexpr int SA = 4;                          // raw A ring (released by the converters)
-  static constexpr int SB = WG ? 10 : 6;                // B ring (released by the MMA)
+#ifndef TC_SA
+#define TC_SA 4
+#endif
+#ifndef TC_SB
+#define TC_SB 6
+#endif
+#ifndef TC_SA_WG
+#define TC_SA_WG 4
+#endif
+#ifndef TC_SB_WG
+#define TC_SB_WG 10
+#endif
+  static constexpr int SA = WG ? TC_SA_WG : TC_SA;      // raw A ring (released by the converters)
+  static constexpr int SB = WG ? TC_SB_WG : TC_SB;      // B ring (released by the MMA)
   static constexpr int A_BYTES = BM * BK * 4;           // raw fp32 A tile, 16 KB
   static constexpr int B_BYTES = (BN / 2) * BK * 4;     // this CTA's half of one B plane, 8 KB
   static constexpr int B_STAGE = 2 * B_BYTES;           // hi + lo planes
