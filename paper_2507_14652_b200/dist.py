@@ -3,7 +3,7 @@
 - chain mode: each rank runs its own chains (global chain ids key Philox); no data-path
   collective.  `chain_ids(rank, C)`.
 - data mode: the training set is sharded by rows (MLP: rows of x/y; DeepONet: condition rows
-  of u/v, trunk inputs replicated); libhmc all-reduces [g_lik, sum r^2] in-graph with NCCL each
+  of u/v, trunk inputs replicated - or, unaligned, the same rows of the per-pair q); libhmc all-reduces [g_lik, sum r^2] in-graph with NCCL each
   leapfrog step and adds the prior once after the reduction.  `shard_rows` cuts
   this rank's block; `broadcast_nccl_id` ships rank 0's NCCL unique id over the process group.
 Marshalling only: no arithmetic of the method lives here.
@@ -39,6 +39,8 @@ def shard_rows(problem, rank: int, world: int):
     lo, hi = row_block(n_c, rank, world)
     sh.u = np.ascontiguousarray(problem.u[lo:hi])
     sh.v = np.ascontiguousarray(problem.v[lo:hi])
+    if np.asarray(problem.q).ndim == 3:  # unaligned DeepONet: each function's own query points
+        sh.q = np.ascontiguousarray(problem.q[lo:hi])
     return sh, n_c * n_x
 
 

@@ -21,6 +21,16 @@ def _free_port():
     return p
 
 
+def _case(kind):
+    if kind == "mlp":
+        arch = ArchSpec("mlp", (NetSpec.plain((2, 7, 5, 1)),))
+        return arch, make_tiny_problem(arch, n=37, active_frac=0.5, seed=3, noise=0.4), 37
+    arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")), has_b0=True)
+    # deeponet_unaligned: per-function query points, sharded with their functions
+    return arch, make_tiny_problem(arch, n_c=11, n_x=9, active_frac=0.6, seed=4, noise=0.4,
+                                   unaligned=(kind == "deeponet_unaligned")), 99
+
+
 def _worker(rank, world, port, kind, q):
     import torch
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -28,13 +38,7 @@ def _worker(rank, world, port, kind, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import hmc as ohmc
     from oracle import network as onet
-    if kind == "mlp":
-        arch = ArchSpec("mlp", (NetSpec.plain((2, 7, 5, 1)),))
-        prob = make_tiny_problem(arch, n=37, active_frac=0.5, seed=3, noise=0.4)
-    else:
-        arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")),
-                        has_b0=True)
-        prob = make_tiny_problem(arch, n_c=11, n_x=9, active_frac=0.6, seed=4, noise=0.4)
+    arch, prob, _ = _case(kind)
     shard, n_global = pdist.shard_rows(prob, rank, world)
     th = prob.frozen[prob.idx].astype(np.float64) + 0.01
     t = ohmc.Target(shard)
@@ -51,7 +55,7 @@ def _worker(rank, world, port, kind, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["mlp", "deeponet"])
+@pytest.mark.parametrize("kind", ["mlp", "deeponet", "deeponet_unaligned"])
 def test_data_mode_reduction_matches_full_batch(kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -65,15 +69,7 @@ def test_data_mode_reduction_matches_full_batch(kind):
         assert p.exitcode == 0
     res.sort(key=lambda r: r[0])
     from oracle import hmc as ohmc
-    if kind == "mlp":
-        arch = ArchSpec("mlp", (NetSpec.plain((2, 7, 5, 1)),))
-        prob = make_tiny_problem(arch, n=37, active_frac=0.5, seed=3, noise=0.4)
-        N = 37
-    else:
-        arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")),
-                        has_b0=True)
-        prob = make_tiny_problem(arch, n_c=11, n_x=9, active_frac=0.6, seed=4, noise=0.4)
-        N = 99
+    arch, prob, N = _case(kind)
     th = prob.frozen[prob.idx].astype(np.float64) + 0.01
     lp_ref, g_ref = ohmc.Target(prob).logp_grad(th)
     for rank, lp, g, n_global, nid in res:
