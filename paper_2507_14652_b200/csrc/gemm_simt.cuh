@@ -41,6 +41,9 @@ struct GemmArgs {
   // tensor-core EPI_WGRAD split over K (ksplit > 1): split s writes its partial k-vector entries
   // to gl_part + s * batch * k (summed in fixed order afterwards)
   int ksplit; float* gl_part;
+  // tensor-core EPI_WGRAD: also reduce this layer's bias gradient from the fused column partials
+  // (bcs[b * s_bcs + blk * M + o], blk < bcs_nblk, fixed order) into gl[b * k + bcs_slot[o]]
+  const float* bcs; int64_t s_bcs; int bcs_nblk; const int32_t* bcs_slot;
   float* gl; int64_t k;
   // EPI_RESID: R = (V - (acc + b0)) * inv_s2; partial sums of r^2 and of R per tile (fp64)
   const float* V; int64_t ldv;

@@ -384,6 +384,11 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
       if (L.ksplit > 1 && x->gl_part) { a.ksplit = L.ksplit; a.gl_part = x->gl_part; }
+      const bool bias_in_gemm = L.bias_active && N.cs_ready;  // (tcgen05 path only)
+      if (bias_in_gemm) {
+        a.bcs_nblk = (int)((L.rows + 31) / 32);
+        a.bcs = N.colsum; a.s_bcs = (int64_t)a.bcs_nblk * L.n_out; a.bcs_slot = x->d_slot + L.b_off;
+      }
       const int id = prof_begin(x, st);
       bool tc = x->tc.accepts(a, false, false);
       if (tc) tc = x->tc.launch(a, false, false, st);
@@ -397,7 +402,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
         prof_end(x, id, st, "tc_wgrad", 2.0 * a.M * a.N * (double)a.K * a.batch,
                  4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
-        if (L.bias_active) {  // bias gradient = column sums of G (fixed order)
+        if (L.bias_active && !bias_in_gemm) {  // bias gradient = column sums of G (fixed order)
           const int id2 = prof_begin(x, st);
           if (N.cs_ready) {  // partials from the producing GEMM's epilogue
             const int nblk = (int)((L.rows + 31) / 32);

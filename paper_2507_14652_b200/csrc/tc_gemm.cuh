@@ -1180,6 +1180,22 @@ __global__ void __launch_bounds__(NT, 1)
       --pend;
     }
     if (lane == 0) bulk_wait0();
+    if (EPI == EPI_WGRAD && a.bcs) {
+      // the layer's bias gradient: every (chain, column) sum of the column partials, spread over
+      // the epilogue threads of all CTAs (replaces a separate reduction launch)
+      const int64_t tot = (int64_t)a.batch * a.M;
+      for (int64_t i = (int64_t)blockIdx.x * (NEPI * 32) + ew * 32 + lane; i < tot; i += (int64_t)gridDim.x * (NEPI * 32)) {
+        const int64_t c = i / a.M;
+        const int o = (int)(i - c * a.M);
+        const int sl = a.bcs_slot[o];
+        if (sl < 0) continue;
+        const float* p = a.bcs + c * a.s_bcs + o;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int blk = 0; blk < a.bcs_nblk; ++blk) acc += p[(int64_t)blk * a.M];
+        a.gl[c * a.k + sl] = acc;
+      }
+    }
   }
   if (mn.prof && lane == 0) {
     if (warp == W_TMA_A) atomicAdd(&g_tcprof[mn.vid][P_TMA_EMPTY], pacc[0]);
