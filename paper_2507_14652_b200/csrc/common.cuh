@@ -120,6 +120,39 @@ __device__ __forceinline__ void tanh_acc2(float& x0, float& x1) {
   x1 = a1 < 0.6f ? s1 : copysignf(b1, x1);
 }
 
+// tanh of a pair with 3 MUFU ops instead of 4 (MUFU / FMA pipes balanced): x0 as tanh_acc,
+// x1 for |x| >= 0.6 as (1 - e) / (1 + e) = Q(e), e = 2^(-2|x| log2 e) in (0, 0.3012], Q a degree-7
+// minimax polynomial (max relative error 1.8e-7 over the range, scripts/micro/tanh_rate.cu)
+__device__ __forceinline__ void tanh_mix2(float& x0, float& x1) {
+  const uint64_t x = pk2(x0, x1);
+  const uint64_t x2 = fmul2(x, x);
+  uint64_t p = ffma2(pk2(-0.005852516740560532f, -0.005852516740560532f), x2,
+                     pk2(0.020753972232341766f, 0.020753972232341766f));
+  p = ffma2(p, x2, pk2(-0.0537688285112381f, -0.0537688285112381f));
+  p = ffma2(p, x2, pk2(0.13331690430641174f, 0.13331690430641174f));
+  p = ffma2(p, x2, pk2(-0.3333328366279602f, -0.3333328366279602f));
+  p = ffma2(p, x2, pk2(1.0f, 1.0f));
+  float s0, s1;
+  upk2(fmul2(p, x), s0, s1);
+  const float a0 = fabsf(x0), a1 = fabsf(x1);
+  float t0, t1;
+  upk2(fmul2(pk2(a0, a1), pk2(2.8853900817779268f, -2.8853900817779268f)), t0, t1);
+  float e0, e1, r0;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(t0));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(t1));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(e0 + 1.0f));
+  const float b0 = fmaf(-2.0f, r0, 1.0f);
+  float q = fmaf(-0.6660300493240356f, e1, 1.4774857759475708f);
+  q = fmaf(q, e1, -1.8797743320465088f);
+  q = fmaf(q, e1, 1.9838345050811768f);
+  q = fmaf(q, e1, -1.998784065246582f);
+  q = fmaf(q, e1, 1.999954104423523f);
+  q = fmaf(q, e1, -1.9999992847442627f);
+  q = fmaf(q, e1, 1.0f);
+  x0 = a0 < 0.6f ? s0 : copysignf(b0, x0);
+  x1 = a1 < 0.6f ? s1 : copysignf(q, x1);
+}
+
 __device__ __forceinline__ float act_fwd(int act, float z) {
   if (act == ACT_TANH) return tanhf(z);
   if (act == ACT_SIN) return sinf(z);

@@ -53,6 +53,9 @@ constexpr int NT = (4 + NCONV + NEPI) * 32;  // 512 threads
 constexpr int W_EPI0 = 0, W_CONV0 = NEPI, W_TMA_A = NEPI + NCONV, W_TMA_B = W_TMA_A + 1, W_MMA = W_TMA_B + 1,
               W_MMA2 = W_MMA + 1;
 constexpr int STG = 4096;  // staging bytes per epilogue warp (32 rows x 32 fp32, 128B swizzle)
+#ifndef TC_TANH2
+#define TC_TANH2 tanh_acc2  // (tanh_mix2: 3 MUFU ops per pair)
+#endif
 #ifndef TC_FOLD
 #define TC_FOLD 2  // K blocks per TMEM accumulator chunk (DESIGN.md §5 "accumulation")
 #endif
@@ -833,13 +836,13 @@ __global__ void __launch_bounds__(NT, 1)
         float4 z0 = srow[q0 ^ (lane & 7)];
         float4 z1 = srow[(q0 + 1) ^ (lane & 7)];
         float4 z2 = (q0 + 2 < 8) ? srow[(q0 + 2) ^ (lane & 7)] : z1;
-        tanh_acc2(z0.x, z0.y);
-        tanh_acc2(z0.z, z0.w);
-        tanh_acc2(z1.x, z1.y);
-        tanh_acc2(z1.z, z1.w);
+        TC_TANH2(z0.x, z0.y);
+        TC_TANH2(z0.z, z0.w);
+        TC_TANH2(z1.x, z1.y);
+        TC_TANH2(z1.z, z1.w);
         if (q0 + 2 < 8) {  // (warp-uniform)
-          tanh_acc2(z2.x, z2.y);
-          tanh_acc2(z2.z, z2.w);
+          TC_TANH2(z2.x, z2.y);
+          TC_TANH2(z2.z, z2.w);
         }
         srow[q0 ^ (lane & 7)] = z0;
         srow[(q0 + 1) ^ (lane & 7)] = z1;
