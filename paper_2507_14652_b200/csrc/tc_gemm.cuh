@@ -161,9 +161,26 @@ __device__ unsigned long long g_tcprof[16][16];  // [kernel variant][slot]
 // 7 converter arrive full_op
 constexpr int TL_N = 256;
 __device__ unsigned long long g_tctl[24][TL_N];
+// try_wait without a suspend-time hint: the thread sleeps for the hardware's own time limit per
+// attempt (fewer issued instructions while waiting; slower wake-up after async-proxy arrivals)
+__device__ __forceinline__ void mbar_wait_block(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, bool on, unsigned long long& acc,
                                             uint32_t hint = 20) {
-  if (!on) { mbar_wait(b, parity, hint); return; }
+  if (!on) {
+    if (hint == 0) mbar_wait_block(b, parity);  // hint 0: blocking form
+    else mbar_wait(b, parity, hint);
+    return;
+  }
   const unsigned long long t0 = clock64();
   mbar_wait(b, parity, hint);
   acc += clock64() - t0;

@@ -1,8 +1,6 @@
 mkdir -p gpurun_out
-for L in libhmc_w0.so libhmc.so libhmc_w2.so; do
-  for D in 0 63; do
-    echo "$L dbg=$D" >> gpurun_out/wait.log
-    HMC_LIB=$PWD/paper_2507_14652_b200/$L HMC_TC_DBG=$D timeout 60 python scripts/tc_timeline.py 2>&1 | head -1 >> gpurun_out/wait.log
-  done
-  HMC_LIB=$PWD/paper_2507_14652_b200/$L timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --breakdown 2>&1 | grep -E "breakdown\] tc|^\{" | cut -c1-120 >> gpurun_out/wait.log
+for H in "20 20 20" "0 20 20" "0 0 20" "0 0 0"; do
+  set -- $H
+  echo "hint p=$1 c=$2 e=$3" >> gpurun_out/wait.log
+  HMC_TC_HINT_P=$1 HMC_TC_HINT_C=$2 HMC_TC_HINT_E=$3 timeout 300 python bench.py --steps 1 --warmup 3 --L 20 --no-cpu-baseline --no-e2e --breakdown 2>&1 | grep -E "breakdown\] tc_(fwd|wgrad|dgrad)|\"value\"" | cut -c1-90 >> gpurun_out/wait.log
 done
