@@ -159,10 +159,21 @@ int hmc_diagnostics(const float* samples, int32_t C, int64_t S, int64_t k, doubl
  * mu.  MLP: N_d = n rows; DeepONet: N_d = n_c * n_x pairs (u_c, y_x).
  * arch / data as for hmc_setup (data targets are not used); mu, sigma_vi [P] fp32 (host or
  * device, sigma_vi >= 0); s2 [P] fp64 out (host or device).  Synchronous: returns when s2 is
- * written.  Ranking and the tau threshold (eqn:threshold) are host logic on s2.
+ * written.  Ranking and the tau threshold (eqn:threshold): hmc_partition.
  * HMC_E_CONFIG on invalid arguments (the same checks as hmc_setup), HMC_E_CUDA / HMC_E_OOM. */
 int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
                     double* s2, void* stream);
+
+/* The tau-partition of the parameters by sensitivity (PAPER.md eqn:threshold P:200-204, §3.2
+ * P:209-212): rank the P values s2 (>= 0) largest first, ties by ascending index, form the
+ * cumulative fraction c_N of the ranked sum and pick N^ - rule 0 ("ge", the text's reading,
+ * DESIGN.md §3): the smallest N with c_N >= tau (1e-15 relative slack); rule 1 ("le", the
+ * equation as printed): the largest N with c_N <= tau.  N^ = 0 when sum s2 <= 0.  Writes the N^
+ * selected flat indices in ascending order to active[0 .. N^) (host or device, capacity P; the
+ * rest untouched) and N^ to *n_hat (host).  s2 [P] fp64 host or device.  Synchronous.
+ * HMC_E_CONFIG unless 1 <= P < 2^31, 0 < tau <= 1, rule in {0, 1}; HMC_E_OOM / HMC_E_CUDA. */
+int hmc_partition(const double* s2, int64_t P, double tau, int32_t rule, int32_t* active, int64_t* n_hat,
+                  void* stream);
 
 /* The dropped constant: -N log(sigma sqrt(2 pi)) - k log(sigma_p sqrt(2 pi)) (N = n_global or
  * n_c x n_x global), so logp + c is S:362's normalised value. */

@@ -76,12 +76,16 @@ def ranking(S2):
 
 
 def cumulative_fraction(S2):
-    """c_n = sum_{i <= n} S^2_(rank i) / sum_j S^2_j, n = 1..N_Theta (eqn:threshold's ratio)."""
+    """c_n = sum_{i <= n} S^2_(rank i) / sum_j S^2_j, n = 1..N_Theta (eqn:threshold's ratio).
+    The denominator is the same ranked running sum at n = N_Theta (left-to-right), so c_N_Theta = 1
+    exactly and every c_n is one sequential sum over one division - a reading that fixes the
+    rounding of the threshold decision ("tau rule")."""
     S2 = np.asarray(S2, dtype=np.float64)
-    tot = S2.sum()
+    cs = np.cumsum(S2[ranking(S2)])
+    tot = cs[-1] if cs.size else 0.0
     if tot <= 0:
         return np.zeros(S2.size)
-    return np.cumsum(S2[ranking(S2)]) / tot
+    return cs / tot
 
 
 def n_hat(S2, tau, rule="ge"):

@@ -56,7 +56,7 @@ EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
            "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict",
-           "hmc_diagnostics"]
+           "hmc_diagnostics", "hmc_partition"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -300,6 +300,22 @@ def hmc_diagnostics(samples, stream=None):
     _check(L.hmc_diagnostics(_ptr(samples, keep, np.float32), C, S, k, rhat.ctypes.data, ess.ctypes.data,
                              _stream(stream)))
     return rhat, ess
+
+
+def hmc_partition(s2, tau: float, rule: str = "ge", stream=None):
+    """Theta_s of eqn:threshold on the GPU: the N^ most sensitive flat indices (ascending int32
+    NumPy array) for sensitivities s2 [P] (NumPy or torch, fp64), rule "ge" (text) or "le"."""
+    keep = []
+    arr = s2 if hasattr(s2, "data_ptr") else np.ascontiguousarray(s2, dtype=np.float64)
+    P = int(arr.shape[0])
+    out = np.empty(P, dtype=np.int32)
+    nh = ctypes.c_int64(0)
+    L = lib()
+    L.hmc_partition.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int32,
+                                ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p]
+    _check(L.hmc_partition(_ptr(arr, keep), P, float(tau), 0 if rule == "ge" else 1, out.ctypes.data,
+                           ctypes.byref(nh), _stream(stream)))
+    return out[:nh.value].copy()
 
 
 def hmc_sensitivity(problem, mu=None, sigma_vi=None, stream=None):

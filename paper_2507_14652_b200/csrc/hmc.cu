@@ -22,6 +22,7 @@
 #include "../../include/hmc.h"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "partition.cuh"
 #include "tc_gemm.cuh"
 
 using namespace hmc;
@@ -1362,6 +1363,67 @@ int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, dou
   CK(cudaStreamSynchronize(x->st));  // temporaries are freed on return
   sync_out(x, us, true, err);
   API_END
+}
+
+int hmc_partition(const double* s2, int64_t P, double tau, int32_t rule, int32_t* active, int64_t* n_hat,
+                  void* stream) {
+  if (!s2 || !active || !n_hat || P < 1 || P > 0x7fffffffLL || !(tau > 0.0 && tau <= 1.0) || (rule != 0 && rule != 1)) {
+    g_err = "config: s2, active, n_hat non-NULL; 1 <= P < 2^31; 0 < tau <= 1; rule 0 (ge) or 1 (le)";
+    return HMC_E_CONFIG;
+  }
+  std::string err;
+  DevBuf tmp;
+  auto tmp_alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    tmp.ptrs.push_back(p);
+    return p;
+  };
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t n2 = 1;
+  while (n2 < P) n2 <<= 1;
+  const int64_t nch = (P + part::CH - 1) / part::CH;
+  double* ds2 = (double*)tmp_alloc((size_t)P * 8);
+  double* key = (double*)tmp_alloc((size_t)n2 * 8);
+  int32_t* idx = (int32_t*)tmp_alloc((size_t)n2 * 4);
+  unsigned long long* res = (unsigned long long*)tmp_alloc(16);
+  int32_t* flag = (int32_t*)tmp_alloc((size_t)P * 4);
+  int64_t* cnt = (int64_t*)tmp_alloc((size_t)(nch + 1) * 8);
+  int32_t* out = (int32_t*)tmp_alloc((size_t)P * 4);
+  if (!ds2 || !key || !idx || !res || !flag || !cnt || !out) { g_err = "cuda: out of device memory"; return HMC_E_OOM; }
+  auto ck = [&](cudaError_t e) { if (e != cudaSuccess && err.empty()) err = cudaGetErrorString(e); };
+  ck(cudaMemcpyAsync(ds2, s2, (size_t)P * 8, cudaMemcpyDefault, st));
+  const unsigned long long init[2] = {(unsigned long long)P, 0ull};
+  ck(cudaMemcpyAsync(res, init, 16, cudaMemcpyHostToDevice, st));
+  ck(cudaMemsetAsync(flag, 0, (size_t)P * 4, st));
+  const unsigned g = (unsigned)std::min<int64_t>((n2 + 255) / 256, 148 * 16);
+  part::k_init<<<g, 256, 0, st>>>(ds2, P, n2, key, idx);
+  for (int64_t kk = 2; kk <= n2; kk <<= 1)
+    for (int64_t j = kk >> 1; j > 0; j >>= 1) part::k_bitonic<<<g, 256, 0, st>>>(key, idx, n2, j, kk);
+  const unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nch + 127) / 128, 148 * 4));
+  double* prefix = ds2;  // (s2 is no longer needed: the keys hold the ranked copy)
+  part::k_prefix_seq<<<1, 1, 0, st>>>(key, P, prefix);
+  unsigned long long hres[2] = {0ull, 0ull};
+  double tot = 0.0;
+  ck(cudaMemcpyAsync(&tot, prefix + P - 1, 8, cudaMemcpyDeviceToHost, st));
+  ck(cudaStreamSynchronize(st));
+  if (tot > 0.0) part::k_nhat_seq<<<g, 256, 0, st>>>(prefix, P, tau, rule, res);
+  ck(cudaMemcpyAsync(hres, res, 16, cudaMemcpyDeviceToHost, st));
+  ck(cudaStreamSynchronize(st));
+  if (!err.empty()) { g_err = "cuda: " + err; return HMC_E_CUDA; }
+  const int64_t nh = !(tot > 0.0) ? 0 : (rule == 0 ? (int64_t)hres[0] : (int64_t)hres[1]);
+  if (nh > 0) {
+    part::k_flags<<<g, 256, 0, st>>>(idx, nh, flag);
+    part::k_flag_count<<<gc, 128, 0, st>>>(flag, P, cnt, nch);
+    part::k_count_scan<<<1, 1, 0, st>>>(cnt, nch);
+    part::k_compact<<<gc, 128, 0, st>>>(flag, P, cnt, nch, out);
+    ck(cudaMemcpyAsync(active, out, (size_t)nh * 4, cudaMemcpyDefault, st));
+  }
+  ck(cudaStreamSynchronize(st));
+  ck(cudaGetLastError());
+  if (!err.empty()) { g_err = "cuda: " + err; return HMC_E_CUDA; }
+  *n_hat = nh;
+  return HMC_OK;
 }
 
 int hmc_diagnostics(const float* samples, int32_t C, int64_t S, int64_t k, double* rhat, double* ess, void* stream) {
