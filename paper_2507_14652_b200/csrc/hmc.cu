@@ -385,7 +385,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
       if (L.ksplit > 1 && x->gl_part) { a.ksplit = L.ksplit; a.gl_part = x->gl_part; }
-      const bool bias_in_gemm = L.bias_active && N.cs_ready;  // (tcgen05 path only)
+      static const bool fuse_bias = !(getenv("HMC_BIAS_FUSE") && atoi(getenv("HMC_BIAS_FUSE")) == 0);
+      const bool bias_in_gemm = fuse_bias && L.bias_active && N.cs_ready;  // (tcgen05 path only)
       if (bias_in_gemm) {
         a.bcs_nblk = (int)((L.rows + 31) / 32);
         a.bcs = N.colsum; a.s_bcs = (int64_t)a.bcs_nblk * L.n_out; a.bcs_slot = x->d_slot + L.b_off;
