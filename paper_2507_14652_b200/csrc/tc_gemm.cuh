@@ -195,42 +195,6 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* m, uint6
       "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
-                                          int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-          su32(dst)),
-      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_pf3(const CUtensorMap* m, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"((uint64_t)m), "r"(c0),
-               "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void tma_pf4(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"((uint64_t)m),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-// multicast variant: the box lands at the same shared offset in every CTA of ctaMask, each
-// CTA's barrier at `bar`'s offset receives the complete_tx
-__device__ __forceinline__ void tma_load3_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
-                                             uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3, %4}], [%5], %6;" ::"r"(su32(dst)),
-      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load4_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
-                                             int c3, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3, %4, %5}], [%6], %7;" ::"r"(su32(dst)),
-      "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(su32(bar)), "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -256,13 +220,6 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_alloc(uint32_t* holder, uint32_t cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(holder)), "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
-}
 // CTA-pair TMEM (one warp of each CTA of the pair executes these)
 __device__ __forceinline__ void tmem_alloc2(uint32_t* holder, uint32_t cols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(holder)), "r"(cols));
@@ -309,27 +266,6 @@ __device__ __forceinline__ void mbar_wait_cl_t(uint64_t* b, uint32_t parity, boo
   mbar_wait_cl(b, parity);
   acc += clock64() - t0;
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-// D[tmem] (+)= A[tmem] . B[smem]: A is M x 8 tf32 (TMEM lane = row, one column per K element)
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum));
-}
 // 32 lanes x 32 consecutive 32-bit columns from registers (lane i of the warp -> TMEM lane base + i)
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -343,18 +279,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// commit arriving on the barrier at `bar`'s offset in every CTA of ctaMask
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   su32(bar)),
-               "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-               : "memory");
-}
 
 // 32 lanes x 16 consecutive 32-bit columns: thread (lane i of the warp) gets TMEM lane
 // (lane base + i), columns [col, col + 16).  Caller waits with tmem_wait_ld().
@@ -407,7 +331,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
 // kernel arguments so the encoding is verified on the device (tests/test_gpu_engine.py).
 struct MnDesc {
   uint32_t lbo = 4096, sbo = 512, layout = 1, kstep = 1024;
-  int pf = 0;    // L2 prefetch distance of the TMA producer, in K blocks (0 = off)
   int prof = 0;  // 1: accumulate per-role wait cycles into g_tcprof[vid]; 2 + v: also record the
                  //    CTA-0 timeline of launches of kernel variant v
   int vid = 0;   // kernel variant (index in tc_variants)
@@ -1307,7 +1230,6 @@ struct TcPlanner {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
     encode = (tc::EncodeTiledFn)fn;
-    if (const char* f = getenv("HMC_TC_PF")) mn.pf = std::max(0, atoi(f));
     if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
