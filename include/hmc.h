@@ -53,6 +53,7 @@ extern "C" {
 enum { HMC_MLP = 0, HMC_DEEPONET = 1 };                          /* P:68, P:369 */
 enum { HMC_ACT_IDENTITY = 0, HMC_ACT_TANH = 1, HMC_ACT_SIN = 2 }; /* P:273, P:335, P:534 */
 enum { HMC_MODE_SINGLE = 0, HMC_MODE_DATA = 1, HMC_MODE_CHAIN = 2 };
+enum { HMC_SHARD_ROWS = 0, HMC_SHARD_POINTS_XB = 1 };
 
 /* A feed-forward net with n_layers linear layers: widths[0] inputs ... widths[n_layers]
  * outputs; layer l applies act[l] to (W_l h + b_l).  Arrays are host memory, read at setup. */
@@ -104,7 +105,12 @@ typedef struct {
   const uint32_t* chain_ids; /* [n_chains] global chain ids keying Philox, or NULL = 0..C-1 */
   int32_t mode;         /* HMC_MODE_*; DATA needs world > 1 ranks sharing one chain set */
   int32_t rank, world;  /* this rank, number of ranks (1 for SINGLE / CHAIN) */
-  const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode only) */
+  int32_t shard;        /* DATA mode layout: HMC_SHARD_ROWS, or HMC_SHARD_POINTS_XB (DeepONet with
+                           shared query points): this rank holds condition block r, u[n_c/world x m],
+                           point block r, q[n_x x d_t], and v[n_c x n_x] for ALL n_c conditions and its
+                           n_x points (hmc_data.n_c = all conditions, n_c % world == 0); the branch
+                           outputs are all-gathered, dB reduce-scattered */
+  const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode, world > 1) */
 } hmc_config;
 
 typedef struct hmc_ctx hmc_ctx;

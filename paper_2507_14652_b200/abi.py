@@ -17,6 +17,7 @@ HMC_OK, HMC_E_CONFIG, HMC_E_CUDA, HMC_E_NCCL, HMC_E_OOM, HMC_E_STATE = 0, 1, 3, 
 HMC_MLP, HMC_DEEPONET = 0, 1
 ACT = {"identity": 0, "tanh": 1, "sin": 2}
 MODE = {"single": 0, "data": 1, "chain": 2}
+SHARD = {"rows": 0, "points_xb": 1}
 
 LIB_PATH = os.environ.get("HMC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
 
@@ -49,7 +50,7 @@ class hmc_config(ctypes.Structure):
                 ("prior_sigma", ctypes.c_double), ("inv_mass", ctypes.c_void_p),
                 ("seed", ctypes.c_uint64), ("n_chains", ctypes.c_int32),
                 ("chain_ids", ctypes.c_void_p), ("mode", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("world", ctypes.c_int32), ("shard", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
@@ -355,7 +356,7 @@ class Context:
 
     def __init__(self, problem, mode: str = "single", rank: int = 0, world: int = 1,
                  nccl_id: Optional[bytes] = None, n_global: int = 0, chain_ids=None,
-                 n_chains: Optional[int] = None):
+                 n_chains: Optional[int] = None, shard: str = "rows"):
         keep = []
         arch = problem.arch
         nets = [(n.widths, n.acts, n.bias) for n in arch.nets]
@@ -369,7 +370,8 @@ class Context:
             d.u = _ptr(problem.u, keep, np.float32)
             d.q = _ptr(problem.q, keep, np.float32)
             d.v = _ptr(problem.v, keep, np.float32)
-            d.n_c, d.n_x = int(problem.u.shape[0]), int(problem.v.shape[1])
+            # n_c = rows of v (all conditions; in the points_xb layout u holds this rank's block)
+            d.n_c, d.n_x = int(problem.v.shape[0]), int(problem.v.shape[1])
             d.q_per_pair = int(len(problem.q.shape) == 3)  # unaligned: q [n_c, n_x, d_t]
         d.n_global = int(n_global)
         c = hmc_config()
@@ -391,6 +393,7 @@ class Context:
         c.chain_ids = _ptr(ids, keep, np.uint32) if ids is not None else None
         c.mode = MODE[mode]
         c.rank, c.world = int(rank), int(world)
+        c.shard = SHARD[shard]
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
             keep.append(idbuf)

@@ -70,6 +70,11 @@ struct hmc_ctx {
   int64_t P = 0, k = 0;
   int64_t n = 0, n_c = 0, n_x = 0, n_global = 0, d_in = 0;
   bool unaligned = false;  // DeepONet with per-pair trunk inputs q[n_c x n_x x d_t] (NEXT-4)
+  // DATA mode, POINTS_XB layout: condition block (n_c_loc = n_c / world rows of u) and point block
+  // (n_x rows of q) per rank; all n_c conditions x this rank's points in v / R
+  bool xb = false;
+  int64_t n_c_loc = 0;
+  float *xb_recv = nullptr, *xb_full = nullptr, *xb_dB = nullptr, *xb_send = nullptr;
   double sigma = 1, sigma_p = 1;
   uint64_t seed = 0;
   bool has_b0 = false;
@@ -500,6 +505,49 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   const LayerInfo& Bl = x->layers[Nb.layers.back()];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Bl.n_out;
+  if (x->xb) {  // POINTS_XB: gather the branch outputs of all conditions, combine with this rank's
+                // points, reduce-scatter dB back to the condition owners, dT stays local
+    std::string& err = x->err;  // (CKN reports through it)
+    const int64_t blk = (int64_t)C * x->n_c_loc * p;
+    CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, st));
+    k_xb_gather<<<148 * 4, 256, 0, st>>>(x->xb_recv, x->xb_full, C, x->world, x->n_c_loc, p);
+    x->launches++;
+    {
+      GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+      a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
+      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+      a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+      a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
+      if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
+      a.inv_s2 = 1.0 / (x->sigma * x->sigma);
+      a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
+      launch_gemm(x, a, true, true, st, "combine");
+    }
+    if (Nb.l_min >= 0) {  // partial dB over this rank's points, all conditions; then reduce-scatter
+      GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
+      a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+      a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
+      a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
+      launch_gemm(x, a, true, false, st, "dB");
+      k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, C, x->world, x->n_c_loc, p);
+      x->launches++;
+      CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, st));
+      Nb.cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
+    }
+    if (Nt.l_min >= 0) {  // dT = R^T B_all, times act' of the trunk output layer: complete locally
+      GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
+      a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+      a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
+      a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
+      a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
+      if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
+      Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+    }
+    if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+    if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    return;
+  }
   if (x->unaligned) {  // per-pair trunk rows: row-wise combine, then the two output gradients
     k_pair_combine<<<dim3((unsigned)x->n_c, C), 256, p * sizeof(float), st>>>(
         Bl.A, Tl.A, p, x->n_c, x->n_x, x->d_v, x->has_b0 ? x->Wd + x->b0_off : nullptr, x->P,
@@ -896,14 +944,23 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->n_c = data->n_c;
     x->n_x = data->n_x;
     x->unaligned = data->q_per_pair != 0;
+    x->xb = cfg->mode == HMC_MODE_DATA && cfg->shard == HMC_SHARD_POINTS_XB;
+    CFG(cfg->shard == HMC_SHARD_ROWS || cfg->shard == HMC_SHARD_POINTS_XB, "shard must be HMC_SHARD_*");
+    if (x->xb) {
+      CFG(!x->unaligned, "POINTS_XB needs shared query points (q_per_pair = 0)");
+      CFG(cfg->world >= 1 && x->n_c % cfg->world == 0, "POINTS_XB needs n_c divisible by world");
+      CFG(arch->net[0].acts[arch->net[0].n_layers - 1] != HMC_ACT_SIN,
+          "POINTS_XB: the branch output layer cannot be sin (its act' is not all-gathered)");
+    }
+    x->n_c_loc = x->xb ? x->n_c / cfg->world : x->n_c;
     const int64_t q_rows = x->unaligned ? x->n_c * x->n_x : x->n_x;
-    hu = to_host(data->u, (size_t)(x->n_c * arch->net[0].widths[0]), err);
+    hu = to_host(data->u, (size_t)(x->n_c_loc * arch->net[0].widths[0]), err);
     hq = to_host(data->q, (size_t)(q_rows * arch->net[1].widths[0]), err);
     hv = to_host(data->v, (size_t)(x->n_c * x->n_x), err);
     for (float v : hu) CFG(std::isfinite(v), "u must be finite");
     for (float v : hq) CFG(std::isfinite(v), "q must be finite");
     for (float v : hv) CFG(std::isfinite(v), "v must be finite");
-    x->nets[0].rows = x->n_c;
+    x->nets[0].rows = x->n_c_loc;
     x->nets[1].rows = q_rows;
   }
   const int64_t n_local = x->kind == HMC_MLP ? x->n : x->n_c * x->n_x;
@@ -1071,6 +1128,13 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->n_part = x->unaligned ? (int)x->n_c
                              : std::max(x->tc.n_tiles(probe, true, true),
                                         (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
+    if (x->xb) {  // all-gather / reduce-scatter staging of the branch outputs and their gradient
+      const size_t blk = (size_t)C * x->n_c_loc * p;
+      x->xb_recv = dalloc<float>(x, blk * x->world, err);
+      x->xb_send = dalloc<float>(x, blk * x->world, err);
+      x->xb_full = dalloc<float>(x, (size_t)C * x->n_c * p, err);
+      x->xb_dB = dalloc<float>(x, (size_t)C * x->n_c * p, err);
+    }
   }
   {  // two-pass column-reduction scratch: max over nets of chunks x (width + 1)
     size_t cap = 0;
@@ -1116,10 +1180,14 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   CK(cudaEventRecord(x->ev_stage, 0));
   CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
   // ---- NCCL (DATA mode) ----
-  if (x->mode == HMC_MODE_DATA && x->world > 1) {
-    CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");
+  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb)) {
     ncclUniqueId id;
-    memcpy(&id, cfg->nccl_id, sizeof(id));
+    if (x->world > 1) {
+      CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");
+      memcpy(&id, cfg->nccl_id, sizeof(id));
+    } else {
+      CKN(ncclGetUniqueId(&id));  // POINTS_XB on one rank: a communicator of one (the collectives run)
+    }
     CKN(ncclCommInitRank(&x->comm, x->world, id, x->rank));
   }
   x->engine = x->tc.describe();

@@ -800,4 +800,24 @@ __global__ void k_pair_dT(const float* __restrict__ R, const float* __restrict__
   }
 }
 
+// ================= DATA mode POINTS_XB layout: rank r owns condition block r ====
+// all-gather result [rank][chain][i][k] -> per-chain rows of all conditions [chain][r*n_loc + i][k]
+__global__ void k_xb_gather(const float* __restrict__ recv, float* __restrict__ full, int C, int G, int64_t n_loc,
+                            int p) {
+  const int64_t per = n_loc * p, total = (int64_t)G * C * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ((int64_t)C * per), rem = t - r * C * per, c = rem / per, e = rem - c * per;
+    full[(c * G + r) * per + e] = recv[t];
+  }
+}
+// per-chain rows of all conditions -> reduce-scatter input [rank][chain][i][k] (block r to rank r)
+__global__ void k_xb_scatter(const float* __restrict__ full, float* __restrict__ send, int C, int G, int64_t n_loc,
+                             int p) {
+  const int64_t per = n_loc * p, total = (int64_t)G * C * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ((int64_t)C * per), rem = t - r * C * per, c = rem / per, e = rem - c * per;
+    send[t] = full[(c * G + r) * per + e];
+  }
+}
+
 }  // namespace hmc

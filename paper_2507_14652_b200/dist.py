@@ -5,7 +5,8 @@
 - data mode: the training set is sharded by rows (MLP: rows of x/y; DeepONet: condition rows
   of u/v, trunk inputs replicated - or, unaligned, the same rows of the per-pair q); libhmc all-reduces [g_lik, sum r^2] in-graph with NCCL each
   leapfrog step and adds the prior once after the reduction.  `shard_rows` cuts
-  this rank's block; `broadcast_nccl_id` ships rank 0's NCCL unique id over the process group.
+  this rank's block; `shard_points_xb` the POINTS_XB condition x point blocks (DeepONet: the
+  branch outputs are all-gathered and dB reduce-scattered in-graph); `broadcast_nccl_id` ships rank 0's NCCL unique id over the process group.
 Marshalling only: no arithmetic of the method lives here.
 """
 from __future__ import annotations
@@ -44,6 +45,21 @@ def shard_rows(problem, rank: int, world: int):
     return sh, n_c * n_x
 
 
+def shard_points_xb(problem, rank: int, world: int):
+    """POINTS_XB layout (DeepONet with shared query points): condition block r of u
+    (n_c / world rows, n_c divisible by world), point block r of q, and v for ALL conditions at
+    those points.  Returns (shard, n_global)."""
+    n_c, n_x = problem.v.shape
+    assert n_c % world == 0, "POINTS_XB needs n_c divisible by world"
+    c0, c1 = row_block(n_c, rank, world)
+    x0, x1 = row_block(n_x, rank, world)
+    sh = copy.copy(problem)
+    sh.u = np.ascontiguousarray(problem.u[c0:c1])
+    sh.q = np.ascontiguousarray(problem.q[x0:x1])
+    sh.v = np.ascontiguousarray(problem.v[:, x0:x1])
+    return sh, n_c * n_x
+
+
 def broadcast_nccl_id(make_id, group=None) -> bytes:
     """Rank 0 calls make_id() (libhmc's hmc_comm_unique_id); every rank returns the same bytes."""
     import torch.distributed as dist
@@ -52,13 +68,17 @@ def broadcast_nccl_id(make_id, group=None) -> bytes:
     return obj[0]
 
 
-def make_context(problem, mode: str, rank: int, world: int, group=None):
-    """libhmc context for this rank: 'chain' (own chains) or 'data' (row shard + NCCL)."""
+def make_context(problem, mode: str, rank: int, world: int, group=None, shard: str = "rows"):
+    """libhmc context for this rank: 'chain' (own chains) or 'data' (row shard, or the POINTS_XB
+    condition x point blocks, + NCCL)."""
     from . import abi
     C = problem.n_chains
-    if mode == "chain" or world == 1:
+    if mode == "chain" or (world == 1 and shard == "rows"):
         return abi.Context(problem, mode="chain" if world > 1 else "single", rank=rank, world=world,
                            chain_ids=chain_ids(rank, C) if world > 1 else None)
-    shard, n_global = shard_rows(problem, rank, world)
-    nid = broadcast_nccl_id(abi.hmc_comm_unique_id, group)
-    return abi.Context(shard, mode="data", rank=rank, world=world, nccl_id=nid, n_global=n_global)
+    if shard == "points_xb":
+        sh, n_global = shard_points_xb(problem, rank, world)
+    else:
+        sh, n_global = shard_rows(problem, rank, world)
+    nid = broadcast_nccl_id(abi.hmc_comm_unique_id, group) if world > 1 else None
+    return abi.Context(sh, mode="data", rank=rank, world=world, nccl_id=nid, n_global=n_global, shard=shard)

@@ -95,3 +95,64 @@ def test_chain_ids_are_global_and_disjoint():
     ids = [set(pdist.chain_ids(r, 64).tolist()) for r in range(8)]
     assert set.union(*ids) == set(range(512))
     assert sum(len(s) for s in ids) == 512
+
+
+def _xb_worker(rank, world, port, q):
+    """POINTS_XB algebra with the oracle's per-net passes: branch on this rank's conditions, trunk
+    on its points, all-gather B, residual for all conditions x its points, reduce-scatter dB,
+    local dT, all-reduce of the likelihood gradient and sum r^2 == the full-batch values."""
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import network as onet
+    arch, prob = _xb_case()
+    sh, n_global = pdist.shard_points_xb(prob, rank, world)
+    th = prob.frozen.astype(np.float64) + 0.01
+    B, tb = onet.net_forward(arch, th, 0, sh.u.astype(np.float64))
+    T, tt = onet.net_forward(arch, th, 1, sh.q.astype(np.float64))
+    parts = [torch.zeros_like(torch.as_tensor(B)) for _ in range(world)]
+    dist.all_gather(parts, torch.as_tensor(B))
+    Ball = torch.cat(parts).numpy()
+    _, b0, _ = onet.layer_table(arch)
+    s2 = prob.noise_sigma ** 2
+    R = sh.v.astype(np.float64) - (Ball @ T.T + th[b0])
+    E = R / s2
+    g = np.zeros_like(th)
+    dB_part = torch.as_tensor(E @ T)                        # all conditions, this rank's points
+    dB_own = torch.zeros_like(torch.as_tensor(B))
+    dist.reduce_scatter(dB_own, list(dB_part.chunk(world)))
+    onet.net_backward(arch, th, 0, tb, dB_own.numpy(), g)   # branch: own conditions
+    onet.net_backward(arch, th, 1, tt, E.T @ Ball, g)       # trunk: own points, all conditions
+    g[b0] += E.sum()
+    buf = torch.tensor(np.concatenate([g, [-np.sum(R * R) / (2 * s2)]]), dtype=torch.float64)
+    dist.all_reduce(buf)
+    q.put((rank, buf.numpy(), n_global))
+    dist.destroy_process_group()
+
+
+def _xb_case():
+    arch = ArchSpec("deeponet", (NetSpec.plain((3, 6, 4)), NetSpec.plain((2, 5, 4), last="tanh")), has_b0=True)
+    return arch, make_tiny_problem(arch, n_c=12, n_x=9, active_frac=0.6, seed=6, noise=0.4)
+
+
+def test_points_xb_exchange_matches_full_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xb_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import network as onet
+    arch, prob = _xb_case()
+    th = prob.frozen.astype(np.float64) + 0.01
+    data = {"u": prob.u.astype(np.float64), "q": prob.q.astype(np.float64), "v": prob.v.astype(np.float64)}
+    ll, g_ref, _ = onet.loglik_grad(arch, th, data, prob.noise_sigma)
+    for rank, buf, n_global in res:
+        assert n_global == 12 * 9
+        np.testing.assert_allclose(buf[:-1], g_ref, rtol=1e-11, atol=1e-11 * np.abs(g_ref).max())
+        assert buf[-1] == pytest.approx(ll, rel=1e-12)
