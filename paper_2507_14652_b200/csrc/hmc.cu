@@ -54,6 +54,9 @@ struct NetInfo {
   float* G[2] = {nullptr, nullptr};
   float* colsum = nullptr;  // [C x ceil(rows/32) x max_w] fused bias-gradient partials
   bool cs_ready = false;    // colsum holds the partials of the current G
+  float* colred = nullptr;       // two-pass column-reduction scratch (own per net: the DeepONet
+  float* narrow_part = nullptr;  // nets run on two streams), narrow-input weight-gradient partials
+  float* gl_part = nullptr;      // K-split weight-gradient partials
 };
 
 struct DevBuf {
@@ -94,7 +97,10 @@ struct hmc_ctx {
   int32_t *d_idx = nullptr, *d_slot = nullptr;
   uint32_t* d_gmask = nullptr;  // per-layer 32-column group masks of the slot map (tc WGRAD epilogue)
   int32_t* d_gbase = nullptr;
-  float* gl_part = nullptr;     // [ksplit_max x C x k] K-split weight-gradient partials
+  // DeepONet (aligned, ROWS): branch and trunk enqueued on two streams inside the graph
+  bool two_streams = false;
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   float* d_inv_mass = nullptr;
   uint32_t* d_chain = nullptr;
   float *cur_theta = nullptr, *cur_grad = nullptr, *wrk_theta = nullptr, *wrk_grad = nullptr, *p = nullptr;
@@ -104,8 +110,6 @@ struct hmc_ctx {
   double *part_sq = nullptr, *part_r = nullptr;
   int n_part = 0;
   float* R = nullptr;
-  float* colred = nullptr;
-  float* narrow_part = nullptr;  // pass-1 partials of the narrow-input weight gradients
   int sq = 0;                    // sensitivity mode (hmc_sensitivity): squared weight-gradient sums
   int colred_chunks = 0;
   double* d_eps = nullptr;   // [C] per-chain step sizes
@@ -169,6 +173,11 @@ struct hmc_ctx {
     if (ev_stage) cudaEventDestroy(ev_stage);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
+    for (int i = 0; i < 2; ++i) {
+      if (ev_fork[i]) cudaEventDestroy(ev_fork[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -322,13 +331,13 @@ void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const f
                          cudaStream_t st) {
   const int nch = (int)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS);
   dim3 grid(nch, x->C);
-#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->narrow_part, nch, x->sq)
+#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->nets[L.net].narrow_part, nch, x->sq)
   switch (L.n_in) {
     case 1: WN(1); break; case 2: WN(2); break; case 3: WN(3); break; case 4: WN(4); break;
     case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;
   }
 #undef WN
-  k_wgrad_narrow_p2<<<x->C, 256, 0, st>>>(x->narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
+  k_wgrad_narrow_p2<<<x->C, 256, 0, st>>>(x->nets[L.net].narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
                                           L.bias ? x->d_slot + L.b_off : nullptr, x->gl, x->k);
   x->launches += 2;
 }
@@ -389,7 +398,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
-      if (L.ksplit > 1 && x->gl_part) { a.ksplit = L.ksplit; a.gl_part = x->gl_part; }
+      if (L.ksplit > 1 && N.gl_part) { a.ksplit = L.ksplit; a.gl_part = N.gl_part; }
       static const bool fuse_bias = !(getenv("HMC_BIAS_FUSE") && atoi(getenv("HMC_BIAS_FUSE")) == 0);
       const bool bias_in_gemm = fuse_bias && L.bias_active && N.cs_ready;  // (tcgen05 path only)
       if (bias_in_gemm) {
@@ -403,7 +412,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         x->launches++;
         if (a.ksplit > 1) {  // fixed-order sum of the splits' partial k-vector entries
           k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.ws_hi - L.ws_lo + 255) / 256, 256)), x->C),
-                            256, 0, st>>>(x->gl_part, a.ksplit, (int64_t)x->C * x->k, x->k, L.ws_lo, L.ws_hi, x->gl);
+                            256, 0, st>>>(N.gl_part, a.ksplit, (int64_t)x->C * x->k, x->k, L.ws_lo, L.ws_hi, x->gl);
           x->launches++;
         }
         x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
@@ -419,8 +428,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
             k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
-                                                             x->colred, chunks, x->sq);
-            k_colred_p2<<<x->C, 256, 0, st>>>(x->colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
+                                                             N.colred, chunks, x->sq);
+            k_colred_p2<<<x->C, 256, 0, st>>>(N.colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
                                               x->k);
             x->launches += 2;
           }
@@ -478,8 +487,8 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     if (N.l_min < 0) return;
     if (O.any_active) {
       dim3 g1(x->colred_chunks, C);
-      k_colred_p1<<<g1, 256, 0, st>>>(x->R, in, s_in, O.rows, O.n_in, x->colred, x->colred_chunks, x->sq);
-      k_colred_p2<<<C, 256, 0, st>>>(x->colred, x->colred_chunks, O.n_in, x->d_slot + O.w_off,
+      k_colred_p1<<<g1, 256, 0, st>>>(x->R, in, s_in, O.rows, O.n_in, N.colred, x->colred_chunks, x->sq);
+      k_colred_p2<<<C, 256, 0, st>>>(N.colred, x->colred_chunks, O.n_in, x->d_slot + O.w_off,
                                      O.bias ? x->d_slot + O.b_off : nullptr, x->gl, x->k);
       x->launches += 2;
     }
@@ -496,10 +505,24 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     return;
   }
   // ---- DeepONet (factored over unique branch / trunk inputs, Q16) ----
-  for (int ni = 0; ni < 2; ++ni) {
-    NetInfo& N = x->nets[ni];
-    for (int i = 0; i < (int)N.layers.size(); ++i) enqueue_forward_hidden(x, N, i, st);
-  }
+  // (two_streams: the branch net's kernels go to a second captured stream, so the short branch
+  // GEMMs fill the trunk GEMMs' last waves; fork / join through events)
+  const bool two = x->two_streams && !x->xb && !x->unaligned;
+  cudaStream_t sb = two ? x->st2 : st;
+  auto fork = [&](int i) {
+    if (!two) return;
+    cudaEventRecord(x->ev_fork[i], st);
+    cudaStreamWaitEvent(sb, x->ev_fork[i], 0);
+  };
+  auto join = [&](int i) {
+    if (!two) return;
+    cudaEventRecord(x->ev_join[i], sb);
+    cudaStreamWaitEvent(st, x->ev_join[i], 0);
+  };
+  fork(0);
+  for (int i = 0; i < (int)x->nets[0].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[0], i, sb);
+  for (int i = 0; i < (int)x->nets[1].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[1], i, st);
+  join(0);
   NetInfo& Nb = x->nets[0];
   NetInfo& Nt = x->nets[1];
   const LayerInfo& Bl = x->layers[Nb.layers.back()];
@@ -583,6 +606,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
     launch_gemm(x, a, true, true, st, "combine");
   }
+  fork(1);
   if (Nb.l_min >= 0) {  // dB = R T, times act' of the branch output layer
     GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
     a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
@@ -590,7 +614,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.C = Nb.G[0]; a.ldc = p; a.sC = x->n_c * p;
     a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = (Bl.act == ACT_SIN) ? Bl.D : Bl.A; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
     if (Bl.bias_active && Nb.colsum) { a.colsum = Nb.colsum; a.s_colsum = (int64_t)((x->n_c + 31) / 32) * p; }
-    Nb.cs_ready = launch_gemm(x, a, true, false, st, "dB") && a.colsum;
+    Nb.cs_ready = launch_gemm(x, a, true, false, sb, "dB") && a.colsum;
   }
   if (Nt.l_min >= 0) {  // dT = R^T B, times act' of the trunk output layer
     GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
@@ -601,8 +625,9 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
     Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
   }
-  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, sb);
   if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+  join(1);
 }
 
 void enqueue_reduce(hmc_ctx* x, cudaStream_t st, std::string& err) {
@@ -1054,7 +1079,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         ks_max = std::max(ks_max, L.ksplit);
       }
     }
-    if (ks_max > 1) x->gl_part = dalloc<float>(x, (size_t)ks_max * x->C * x->k, err);
+    if (ks_max > 1)
+      for (int ni = 0; ni < x->n_nets; ++ni) x->nets[ni].gl_part = dalloc<float>(x, (size_t)ks_max * x->C * x->k, err);
     x->d_gmask = dalloc<uint32_t>(x, gm.size(), err);
     x->d_gbase = dalloc<int32_t>(x, gb.size(), err);
     if (!gm.empty()) {
@@ -1142,7 +1168,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       const size_t chunks = (size_t)((x->nets[ni].rows + COLRED_CH - 1) / COLRED_CH);
       cap = std::max(cap, chunks * (size_t)(x->nets[ni].max_w + 1));
     }
-    x->colred = dalloc<float>(x, (size_t)C * cap, err);
+    for (int ni = 0; ni < x->n_nets; ++ni) x->nets[ni].colred = dalloc<float>(x, (size_t)C * cap, err);
   }
   {  // narrow-input weight-gradient partials: max over narrow layers of chunks x n_out x (n_in + 1)
     size_t cap = 0;
@@ -1152,7 +1178,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         if (is_narrow(L))
           cap = std::max(cap, (size_t)((x->nets[ni].rows + NARROW_ROWS - 1) / NARROW_ROWS) * L.n_out * (L.n_in + 1));
       }
-    x->narrow_part = dalloc<float>(x, (size_t)C * cap, err);
+    for (int ni = 0; ni < x->n_nets; ++ni) x->nets[ni].narrow_part = dalloc<float>(x, (size_t)C * cap, err);
   }
   x->part_sq = dalloc<double>(x, (size_t)C * x->n_part, err);
   x->part_r = dalloc<double>(x, (size_t)C * x->n_part, err);
@@ -1179,6 +1205,17 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   CK(cudaEventCreateWithFlags(&x->ev_out, cudaEventDisableTiming));
   CK(cudaEventRecord(x->ev_stage, 0));
   CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
+  {
+    const char* e = getenv("HMC_STREAMS");
+    x->two_streams = x->kind == HMC_DEEPONET && !x->unaligned && !x->xb && !(e && atoi(e) == 1);
+    if (x->two_streams) {
+      CK(cudaStreamCreateWithFlags(&x->st2, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&x->ev_fork[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&x->ev_join[i], cudaEventDisableTiming));
+      }
+    }
+  }
   // ---- NCCL (DATA mode) ----
   if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb)) {
     ncclUniqueId id;
