@@ -51,8 +51,13 @@ struct NetInfo {
   int64_t rows = 0;
   const float* input = nullptr;
   int max_w = 0;
-  float* G[2] = {nullptr, nullptr};
-  float* colsum = nullptr;  // [C x ceil(rows/32) x max_w] fused bias-gradient partials
+  float* G[3] = {nullptr, nullptr, nullptr};  // gradient buffers (3 rotate when wgrads run on ws)
+  float* colsum = nullptr;  // [C x ceil(rows/32) x max_w] fused bias-gradient partials (layer top)
+  float* cs[3] = {nullptr, nullptr, nullptr};  // per-layer rotation of colsum (cs[i % 3] = layer i)
+  // weight gradients on their own captured stream ws, overlapping the input-gradient chain:
+  // evA[i] = delta_i (and its bias partials) ready, evW[i] = wgrad(i) done
+  cudaStream_t ws = nullptr;
+  std::vector<cudaEvent_t> evA, evW;
   bool cs_ready = false;    // colsum holds the partials of the current G
   float* colred = nullptr;       // two-pass column-reduction scratch (own per net: the DeepONet
   float* narrow_part = nullptr;  // nets run on two streams), narrow-input weight-gradient partials
@@ -178,6 +183,11 @@ struct hmc_ctx {
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
     }
     if (st2) cudaStreamDestroy(st2);
+    for (auto& N : nets) {
+      for (auto e : N.evA) cudaEventDestroy(e);
+      for (auto e : N.evW) cudaEventDestroy(e);
+      if (N.ws) cudaStreamDestroy(N.ws);
+    }
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -377,12 +387,23 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
 }
 
 // backward through layers i = top .. l_min of a net; G of layer `top` is in N.G[cur]
-void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t st) {
+void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t ms) {
+  // ws: the weight-gradient stream (N.ws, when this net's backward runs with overlap) - wgrad(i)
+  // starts when delta_i is ready (evA[i]) and runs beside dgrad(i) and dgrad(i - 1); dgrad(i)
+  // writes the gradient / bias-partial buffers last read by wgrad(i + 2), so it waits for evW[i + 2]
+  const bool ov = N.ws != nullptr && N.G[2] != nullptr && (int)N.evA.size() > top;
   for (int i = top; i >= N.l_min; --i) {
     LayerInfo& L = x->layers[N.layers[i]];
     const float* G = N.G[cur];
     int64_t s_in;
     const float* in = layer_input(x, N, i, &s_in);
+    cudaStream_t st = ms;
+    if (ov) {
+      cudaEventRecord(N.evA[i], ms);
+      cudaStreamWaitEvent(N.ws, N.evA[i], 0);
+      st = N.ws;
+    }
+    float* cs_i = ov ? N.cs[i % 3] : N.colsum;  // this layer's bias partials
     if (L.any_active && is_narrow(L)) {
       const int id = prof_begin(x, st);
       launch_wgrad_narrow(x, L, G, in, s_in, st);
@@ -403,7 +424,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       const bool bias_in_gemm = fuse_bias && L.bias_active && N.cs_ready;  // (tcgen05 path only)
       if (bias_in_gemm) {
         a.bcs_nblk = (int)((L.rows + 31) / 32);
-        a.bcs = N.colsum; a.s_bcs = (int64_t)a.bcs_nblk * L.n_out; a.bcs_slot = x->d_slot + L.b_off;
+        a.bcs = cs_i; a.s_bcs = (int64_t)a.bcs_nblk * L.n_out; a.bcs_slot = x->d_slot + L.b_off;
       }
       const int id = prof_begin(x, st);
       bool tc = x->tc.accepts(a, false, false);
@@ -423,7 +444,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           if (N.cs_ready) {  // partials from the producing GEMM's epilogue
             const int nblk = (int)((L.rows + 31) / 32);
             k_colsum_reduce<<<dim3((unsigned)((L.n_out + 31) / 32), x->C), 1024, 0, st>>>(
-                N.colsum, (int64_t)nblk * L.n_out, nblk, L.n_out, x->d_slot + L.b_off, x->gl, x->k);
+                cs_i, (int64_t)nblk * L.n_out, nblk, L.n_out, x->d_slot + L.b_off, x->gl, x->k);
             x->launches += 1;
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
@@ -443,21 +464,27 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
                  4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
       }
     }
+    if (ov) cudaEventRecord(N.evW[i], N.ws);
     if (i > N.l_min) {
+      st = ms;
+      const int nxt = ov ? (cur + 1) % 3 : (cur ^ 1);
+      if (ov && i + 2 <= top) cudaStreamWaitEvent(ms, N.evW[i + 2], 0);  // buffers of delta_{i+2}
       const LayerInfo& Pv = x->layers[N.layers[i - 1]];
       GemmArgs a = gemm_base((int)L.rows, L.n_in, L.n_out, x->C);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
       a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
-      a.C = N.G[cur ^ 1]; a.ldc = L.n_in; a.sC = L.rows * L.n_in;
+      a.C = N.G[nxt]; a.ldc = L.n_in; a.sC = L.rows * L.n_in;
       a.epi = EPI_DACT; a.act = Pv.act;
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
       PreSplit pre;
       if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc; }
-      if (Pv.bias_active && N.colsum) { a.colsum = N.colsum; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
+      float* cs_prev = ov ? N.cs[(i - 1) % 3] : N.colsum;
+      if (Pv.bias_active && cs_prev) { a.colsum = cs_prev; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
       N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
-      cur ^= 1;
+      cur = nxt;
     }
   }
+  if (ov) cudaStreamWaitEvent(ms, N.evW[N.l_min], 0);  // all weight gradients done (stream order)
 }
 
 // forward + backward of one full-batch gradient evaluation (likelihood part only)
@@ -978,6 +1005,10 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
           "POINTS_XB: the branch output layer cannot be sin (its act' is not all-gathered)");
     }
     x->n_c_loc = x->xb ? x->n_c / cfg->world : x->n_c;
+    {
+      const char* e = getenv("HMC_STREAMS");
+      x->two_streams = !x->unaligned && !x->xb && !(e && atoi(e) == 1);
+    }
     const int64_t q_rows = x->unaligned ? x->n_c * x->n_x : x->n_x;
     hu = to_host(data->u, (size_t)(x->n_c_loc * arch->net[0].widths[0]), err);
     hq = to_host(data->q, (size_t)(q_rows * arch->net[1].widths[0]), err);
@@ -1196,6 +1227,21 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       N.G[0] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       N.G[1] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       if (x->tc.enabled) N.colsum = dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err);
+      if (x->two_streams) {  // overlapped weight gradients: a third gradient buffer, rotated partials
+        N.G[2] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
+        const int top = nl - 1;
+        for (int r = 0; r < 3; ++r)
+          N.cs[r] = (r == top % 3) ? N.colsum
+                                   : (x->tc.enabled ? dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err)
+                                                    : nullptr);
+        CK(cudaStreamCreateWithFlags(&N.ws, cudaStreamNonBlocking));
+        N.evA.resize(nl);
+        N.evW.resize(nl);
+        for (int i = 0; i < nl; ++i) {
+          CK(cudaEventCreateWithFlags(&N.evA[i], cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&N.evW[i], cudaEventDisableTiming));
+        }
+      }
     }
   }
   CK(cudaMallocHost((void**)&x->h_rec, sizeof(Rec)));
@@ -1206,8 +1252,6 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   CK(cudaEventRecord(x->ev_stage, 0));
   CK(cudaStreamCreateWithFlags(&x->st, cudaStreamNonBlocking));
   {
-    const char* e = getenv("HMC_STREAMS");
-    x->two_streams = x->kind == HMC_DEEPONET && !x->unaligned && !x->xb && !(e && atoi(e) == 1);
     if (x->two_streams) {
       CK(cudaStreamCreateWithFlags(&x->st2, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
