@@ -104,6 +104,7 @@ struct hmc_ctx {
   int32_t* d_gbase = nullptr;
   // DeepONet (aligned, ROWS): branch and trunk enqueued on two streams inside the graph
   bool two_streams = false;
+  bool wgrad_ov = false;  // weight gradients on their own stream per net (any layout but xb / unaligned)
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   float* d_inv_mass = nullptr;
@@ -991,6 +992,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (float v : hx) CFG(std::isfinite(v), "x must be finite");
     for (float v : hy) CFG(std::isfinite(v), "y must be finite");
     x->nets[0].rows = x->n;
+    const char* e = getenv("HMC_STREAMS");
+    x->wgrad_ov = !(e && atoi(e) == 1);
   } else {
     CFG(data->u && data->q && data->v && data->n_c >= 1 && data->n_x >= 1, "DeepONet data needs u, q, v, n_c, n_x >= 1");
     x->n_c = data->n_c;
@@ -1008,6 +1011,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     {
       const char* e = getenv("HMC_STREAMS");
       x->two_streams = !x->unaligned && !x->xb && !(e && atoi(e) == 1);
+      x->wgrad_ov = x->two_streams;
     }
     const int64_t q_rows = x->unaligned ? x->n_c * x->n_x : x->n_x;
     hu = to_host(data->u, (size_t)(x->n_c_loc * arch->net[0].widths[0]), err);
@@ -1227,7 +1231,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       N.G[0] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       N.G[1] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       if (x->tc.enabled) N.colsum = dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err);
-      if (x->two_streams) {  // overlapped weight gradients: a third gradient buffer, rotated partials
+      if (x->wgrad_ov) {  // overlapped weight gradients: a third gradient buffer, rotated partials
         N.G[2] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
         const int top = nl - 1;
         for (int r = 0; r < 3; ++r)
