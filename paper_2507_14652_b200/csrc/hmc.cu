@@ -392,7 +392,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
   // ws: the weight-gradient stream (N.ws, when this net's backward runs with overlap) - wgrad(i)
   // starts when delta_i is ready (evA[i]) and runs beside dgrad(i) and dgrad(i - 1); dgrad(i)
   // writes the gradient / bias-partial buffers last read by wgrad(i + 2), so it waits for evW[i + 2]
-  const bool ov = N.ws != nullptr && N.G[2] != nullptr && (int)N.evA.size() > top;
+  const bool ov = N.ws != nullptr && N.G[2] != nullptr && (int)N.evA.size() > top && !x->prof_armed;
   for (int i = top; i >= N.l_min; --i) {
     LayerInfo& L = x->layers[N.layers[i]];
     const float* G = N.G[cur];
@@ -535,7 +535,8 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   // ---- DeepONet (factored over unique branch / trunk inputs, Q16) ----
   // (two_streams: the branch net's kernels go to a second captured stream, so the short branch
   // GEMMs fill the trunk GEMMs' last waves; fork / join through events)
-  const bool two = x->two_streams && !x->xb && !x->unaligned;
+  // (the profiled step - prof_armed - runs on one stream, so each kernel is timed alone)
+  const bool two = x->two_streams && !x->xb && !x->unaligned && !x->prof_armed;
   cudaStream_t sb = two ? x->st2 : st;
   auto fork = [&](int i) {
     if (!two) return;
