@@ -1039,7 +1039,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
-          if (a.act != ACT_ID) {
+          if (a.act != ACT_ID && !(mn.dbg & 128)) {  // (128: dev experiment, no act' product)
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const float4 d4 = srow[q ^ (lane & 7)];
