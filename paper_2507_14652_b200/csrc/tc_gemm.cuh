@@ -340,7 +340,7 @@ struct MnDesc {
   // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
   int btrunc = 1;
   int pdl = 1;       // programmatic dependent launch (HMC_TC_PDL=0 disables)
-  int tanh_end = 0;  // EPI_FWD tanh in registers at the tile end (1) or in emit steps (0): equal speed (measured)
+  int tanh_end = 1;  // EPI_FWD tanh in registers at the tile end (1; +1 % with concurrent streams) or in emit steps (0)
   // mbarrier try_wait suspend-time hints (ns) of the producers / converters / epilogue waits: a
   // spinning waiter takes issue slots from the working warps of its SM sub-partition
   uint32_t hint_p = 20, hint_c = 20, hint_e = 20;
