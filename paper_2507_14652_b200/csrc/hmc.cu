@@ -348,7 +348,8 @@ void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const f
     case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;
   }
 #undef WN
-  k_wgrad_narrow_p2<<<x->C, 256, 0, st>>>(x->nets[L.net].narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
+  k_wgrad_narrow_p2<<<dim3((unsigned)((L.n_out * (L.n_in + 1) + 255) / 256), x->C), 256, 0, st>>>(
+      x->nets[L.net].narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
                                           L.bias ? x->d_slot + L.b_off : nullptr, x->gl, x->k);
   x->launches += 2;
 }

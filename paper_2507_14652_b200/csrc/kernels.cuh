@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X,
                                                     const float* __restrict__ Wd, int64_t P, int64_t w_off,
                                                     int64_t b_off, int act, float* __restrict__ A,
                                                     float* __restrict__ D) {
-  __shared__ float xs[NARROW_ROWS * DIN];
+  __shared__ __align__(16) float xs[NARROW_ROWS * DIN];
   const int c = blockIdx.y;
   const int64_t r0 = (int64_t)blockIdx.x * NARROW_ROWS;
   const int nr = (int)min((int64_t)NARROW_ROWS, rows - r0);
@@ -216,9 +216,20 @@ __global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X,
       float z[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        float xr[DIN];
+        if (DIN % 4 == 0) {  // broadcast row of X as float4 loads
+#pragma unroll
+          for (int i = 0; i < DIN; i += 4) {
+            const float4 x4 = *reinterpret_cast<const float4*>(xs + (r + u) * DIN + i);
+            xr[i] = x4.x; xr[i + 1] = x4.y; xr[i + 2] = x4.z; xr[i + 3] = x4.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < DIN; ++i) xr[i] = xs[(r + u) * DIN + i];
+        }
         z[u] = bias;
 #pragma unroll
-        for (int i = 0; i < DIN; ++i) z[u] = fmaf(xs[(r + u) * DIN + i], w[i], z[u]);
+        for (int i = 0; i < DIN; ++i) z[u] = fmaf(xr[i], w[i], z[u]);
       }
       if (dout) {
 #pragma unroll
@@ -250,12 +261,15 @@ template <int DIN>
 __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict__ G, int64_t sG, const float* __restrict__ X,
                                                          int64_t sX, int64_t rows, int n_out, float* __restrict__ part,
                                                          int n_chunks, int sq) {
-  __shared__ float xs[NARROW_ROWS * DIN];
+  __shared__ __align__(16) float xs[NARROW_ROWS * DIN];
   const int c = blockIdx.y, ch = blockIdx.x;
   const int64_t r0 = (int64_t)ch * NARROW_ROWS;
   const int nr = (int)min((int64_t)NARROW_ROWS, rows - r0);
   const float* Xc = X + (int64_t)c * sX + r0 * DIN;
-  for (int t = threadIdx.x; t < nr * DIN; t += blockDim.x) xs[t] = Xc[t];
+  for (int t = threadIdx.x; t < nr * DIN; t += blockDim.x) {
+    const float xv = Xc[t];
+    xs[t] = sq ? xv * xv : xv;  // sensitivity mode: sum G^2 X^2 and sum G^2
+  }
   __syncthreads();
   for (int o = threadIdx.x; o < n_out; o += blockDim.x) {
     float acc[DIN + 1];
@@ -265,12 +279,20 @@ __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict
 #pragma unroll 8
     for (int r = 0; r < nr; ++r) {  // (unrolled: 8 loads of G in flight per thread)
       float gv = g[(int64_t)r * n_out];
-      if (sq) gv *= gv;   // sensitivity mode: sum G^2 X^2 and sum G^2
+      if (sq) gv *= gv;
+      float xr[DIN];
+      if (DIN % 4 == 0) {  // broadcast row of X as float4 loads
 #pragma unroll
-      for (int i = 0; i < DIN; ++i) {
-        const float xv = xs[r * DIN + i];
-        acc[i] = fmaf(gv, sq ? xv * xv : xv, acc[i]);
+        for (int i = 0; i < DIN; i += 4) {
+          const float4 x4 = *reinterpret_cast<const float4*>(xs + r * DIN + i);
+          xr[i] = x4.x; xr[i + 1] = x4.y; xr[i + 2] = x4.z; xr[i + 3] = x4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < DIN; ++i) xr[i] = xs[r * DIN + i];
       }
+#pragma unroll
+      for (int i = 0; i < DIN; ++i) acc[i] = fmaf(gv, xr[i], acc[i]);
       acc[DIN] += gv;
     }
     float* pp = part + (((int64_t)c * n_chunks + ch) * n_out + o) * (DIN + 1);
@@ -280,17 +302,21 @@ __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict
 }
 
 // pass 2: fixed-order sum over chunks, compaction into the k-vector (W[o][i] at o*DIN + i)
+// (grid: (entries / 256, chains); one (o, i) entry per thread, chunks summed in order with 8
+//  loads in flight)
 __global__ void k_wgrad_narrow_p2(const float* __restrict__ part, int n_chunks, int n_out, int din,
                                   const int32_t* __restrict__ slot_w, const int32_t* __restrict__ slot_b,
                                   float* __restrict__ gl, int64_t k) {
-  const int c = blockIdx.x;
+  const int c = blockIdx.y;
   const int per = n_out * (din + 1);
-  for (int t = threadIdx.x; t < per; t += blockDim.x) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < per; t += gridDim.x * blockDim.x) {
     const int o = t / (din + 1), i = t - o * (din + 1);
     const int sl = (i < din) ? slot_w[o * din + i] : (slot_b ? slot_b[o] : -1);
     if (sl < 0) continue;
     float acc = 0.f;
-    for (int ch = 0; ch < n_chunks; ++ch) acc += part[((int64_t)c * n_chunks + ch) * per + t];
+    const float* p = part + (int64_t)c * n_chunks * per + t;
+#pragma unroll 8
+    for (int ch = 0; ch < n_chunks; ++ch) acc += p[(int64_t)ch * per];
     gl[(int64_t)c * k + sl] = acc;
   }
 }
