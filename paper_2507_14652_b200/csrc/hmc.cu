@@ -1188,9 +1188,11 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     probe.lda = p; probe.sA = x->n_c * p; probe.ldb = p; probe.sB = x->n_x * p;
     const int bm = pick_bm((int)x->n_c, (int)x->n_x);
     // partial slots: max over both engines (unused slots stay zero); unaligned: one per function
+    // (tcgen05: one slot per tile and epilogue warp)
+    const int tc_slots = (int)(((x->n_c + tc::BM - 1) / tc::BM) * ((x->n_x + TcPlanner::BN - 1) / TcPlanner::BN)) * tc::NEPI;
     x->n_part = x->unaligned ? (int)x->n_c
-                             : std::max(x->tc.n_tiles(probe, true, true),
-                                        (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
+                             : std::max(tc_slots, (int)(((x->n_x + bm - 1) / bm) * ((x->n_c + bm - 1) / bm)));
+    (void)probe;
     if (x->xb) {  // all-gather / reduce-scatter staging of the branch outputs and their gradient
       const size_t blk = (size_t)C * x->n_c_loc * p;
       x->xb_recv = dalloc<float>(x, blk * x->world, err);

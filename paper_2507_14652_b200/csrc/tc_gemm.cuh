@@ -409,7 +409,6 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* xfull = tempty + NACC;                // [NEPI] per epilogue warp: mX tiles landed
   uint64_t* bsplit = xfull + NEPI;                // [SB]   epilogue (raw B split) -> MMA (ESPLIT)
   uint32_t* tmem_holder = (uint32_t*)(bsplit + SB);
-  double* red = (double*)(bsplit + SB + 1);       // [2 x NEPI] epilogue reductions
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
@@ -1100,20 +1099,17 @@ __global__ void __launch_bounds__(NT, 1)
       if (tt) g_tctl[22][jc - 1] = clock64();
       if (mn.prof) pacc[2] += clock64() - t_out0;
       if (EPI == EPI_RESID) {
-        // deterministic 256-thread reduction: warp shuffles, then fixed-order sum of 8 warps
+        // deterministic: warp shuffles, then one partial per (tile, epilogue warp) - slot
+        // rem * NEPI + ew - summed in fixed order by the reduction kernel (no barrier across
+        // the epilogue warps per tile)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           psq += __shfl_down_sync(0xffffffffu, psq, o);
           pr += __shfl_down_sync(0xffffffffu, pr, o);
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (lane == 0) { red[ew] = psq; red[NEPI + ew] = pr; }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (ew == 0 && lane == 0 && mt < n_mt) {
-          double sq = 0.0, sr = 0.0;
-          for (int w = 0; w < NEPI; ++w) { sq += red[w]; sr += red[NEPI + w]; }
-          a.part_sq[(int64_t)b * a.n_part + rem] = sq;
-          a.part_r[(int64_t)b * a.n_part + rem] = sr;
+        if (lane == 0 && mt < n_mt) {
+          a.part_sq[(int64_t)b * a.n_part + (int64_t)rem * NEPI + ew] = psq;
+          a.part_r[(int64_t)b * a.n_part + (int64_t)rem * NEPI + ew] = pr;
         }
       }
     }
@@ -1296,10 +1292,6 @@ struct TcPlanner {
     return (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch;
   }
 
-  int n_tiles(const GemmArgs& a, bool akm, bool bkm) const {
-    if (!accepts(a, akm, bkm)) return -1;
-    return ((a.M + tc::BM - 1) / tc::BM) * ((a.N + BN - 1) / BN);
-  }
 
   const char* describe() const { return enabled ? "tcgen05-3xtf32+simt" : "simt"; }
 
