@@ -96,7 +96,7 @@ struct hmc_ctx {
   float *d_x = nullptr, *d_y = nullptr, *d_u = nullptr, *d_q = nullptr, *d_v = nullptr;
   float* Wd = nullptr;
   float *Whi = nullptr, *Wlo = nullptr;
-  int64_t* d_tcpos = nullptr;
+  int32_t* d_tcpos = nullptr;
   int64_t Ptc = 0;
   int colred_cap = 0;
   int32_t *d_idx = nullptr, *d_slot = nullptr;
@@ -1041,7 +1041,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   if (x->has_b0) x->b0_slot = slot[x->b0_off];
   // ---- tensor-core engine: which layers keep tf32 hi/lo weight planes ----
   x->tc.init();
-  std::vector<int64_t> tcpos((size_t)x->k, -1);
+  std::vector<int32_t> tcpos((size_t)x->k, -1);
   if (x->tc.enabled) {
     for (int ni = 0; ni < x->n_nets; ++ni) {
       NetInfo& N = x->nets[ni];
@@ -1058,7 +1058,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (int64_t j = 0; j < x->k; ++j)
       for (auto& L : x->layers)
         if (L.tc_w && h_idx[j] >= L.w_off && h_idx[j] < L.w_off + (int64_t)L.n_in * L.n_out)
-          tcpos[j] = L.q_off + (h_idx[j] - L.w_off);
+          tcpos[j] = (int32_t)(L.q_off + (h_idx[j] - L.w_off));
   }
   for (int ni = 0; ni < x->n_nets; ++ni) {
     NetInfo& N = x->nets[ni];
@@ -1139,8 +1139,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     // HMC_TC_RAWB=1: one raw plane split in shared memory by the converters (half the L2
     // traffic, measured 2-3 % slower: the converters are on the critical path)
     if (!getenv("HMC_TC_RAWB")) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
-    x->d_tcpos = dalloc<int64_t>(x, x->k, err);
-    CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 8, cudaMemcpyHostToDevice));
+    x->d_tcpos = dalloc<int32_t>(x, x->k, err);
+    CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 4, cudaMemcpyHostToDevice));
     for (auto& L : x->layers)
       if (L.tc_w)
         k_split_layer<<<148 * 4, 256>>>(x->Wd, x->P, L.w_off, (int64_t)L.n_in * L.n_out, x->Whi, x->Wlo, x->Ptc,

@@ -28,7 +28,7 @@ struct KState {
   float* Wd;                   // [C x P] dense per-chain parameters (frozen mu + active theta)
   float* Whi; float* Wlo;      // [C x Ptc] the tensor-core layers' weights: one raw plane (Wlo = nullptr)
                                // or tf32 hi / lo planes; 16B-aligned rows for TMA
-  const int64_t* tcpos;        // [k] position of active entry j in the planes, -1 if none
+  const int32_t* tcpos;        // [k] position of active entry j in the planes, -1 if none
   int64_t Ptc;
   float* cur_theta; float* cur_grad; double* cur_logp;   // chain state (the cache)
   float* wrk_theta; float* wrk_grad; double* wrk_logp;   // trajectory working state
@@ -47,9 +47,9 @@ constexpr int KT = 256;  // threads of the per-chain state kernels
 
 // theta_j of chain c -> dense parameters (and the tf32 hi/lo planes of tensor-core layers)
 __device__ __forceinline__ void put_param(const KState& s, int64_t c, int64_t j, float th) {
-  s.Wd[c * s.P + s.idx[j]] = th;
+  s.Wd[c * s.P + __ldg(s.idx + j)] = th;
   if (s.tcpos) {
-    const int64_t q = s.tcpos[j];
+    const int64_t q = __ldg(s.tcpos + j);
     if (q >= 0) {
       if (s.Wlo) {  // pre-split hi / lo planes
         const float h = tf32_hi(th);
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(256) k_leapfrog(KState s) {
     float th = s.wrk_theta[t];
     const float g = s.gl[t] - (float)((double)th * s.inv_sp2);
     s.wrk_grad[t] = g;
-    const float im = s.inv_mass ? s.inv_mass[j] : 1.f;
+    const float im = s.inv_mass ? __ldg(s.inv_mass + j) : 1.f;
     const float p = fmaf(fe, g, s.p[t]);
     s.p[t] = p;
     th = fmaf(fe * im, p, th);
