@@ -404,3 +404,33 @@ def test_config_errors_are_reported():
         lp, g = gpu_grad(c, th)
         with pytest.raises(abi.HmcError):
             abi.hmc_trajectory(c.ctx, th, lp, g, -1.0, 5, 0)
+
+
+@pytest.mark.parametrize("name", ["mlp_ragged", "deeponet_ragged"])
+def test_host_buffers_equal_device_buffers(name):
+    """The end-to-end path (hmc_sample on pinned / pageable host buffers, the bench's e2e) gives
+    bitwise the same samples, decisions, energies and final state as device buffers."""
+    torch = torch_cuda()
+    from paper_2507_14652_b200 import abi
+    arch, kw = TINY[name]
+    prob = make_tiny_problem(arch, n_chains=3, seed=9, noise=0.3, **kw)
+    th = jittered_states(prob, 3, scale=0.005)
+    S, L, eps = 4, 6, 5e-4
+    with _ctx(prob) as c:
+        lp, g = gpu_grad(c, th)
+        T, LP, G = to_dev(th, torch.float32), to_dev(lp, torch.float64), to_dev(g, torch.float32)
+        smp = torch.empty(3, S, prob.k, device="cuda")
+        a = torch.empty(3, S, dtype=torch.uint8, device="cuda")
+        d = torch.empty(3, S, dtype=torch.float64, device="cuda")
+        abi.hmc_sample(c.ctx, T, LP, G, eps, L, 11, S, smp, a, d)
+        torch.cuda.synchronize()
+        hT, hLP, hG = th.copy(), lp.copy(), g.copy()
+        hs = np.empty((3, S, prob.k), dtype=np.float32)
+        ha = np.empty((3, S), dtype=np.uint8)
+        hd = np.empty((3, S), dtype=np.float64)
+        abi.hmc_sample(c.ctx, hT, hLP, hG, eps, L, 11, S, hs, ha, hd)
+    np.testing.assert_array_equal(hs, smp.cpu().numpy())
+    np.testing.assert_array_equal(ha, a.cpu().numpy())
+    np.testing.assert_array_equal(hd, d.cpu().numpy())
+    np.testing.assert_array_equal(hT, T.cpu().numpy())
+    np.testing.assert_array_equal(hG, G.cpu().numpy())
