@@ -36,6 +36,7 @@ struct LayerInfo {
   bool bias = false, any_active = false;
   int64_t w_off = 0, b_off = -1, rows = 0;
   bool tc_w = false;          // weights kept as tf32 hi/lo planes for the tensor-core engine
+  bool planes_only = false;   // ... and only there: the leapfrog scatter skips the dense copy
   bool bias_active = false;
   int64_t q_off = 0;           // offset of this layer's weights in the hi/lo planes
   int64_t g_off = -1;          // offset of this layer's [n_out x ceil(n_in/32)] group masks (d_gmask)
@@ -314,6 +315,10 @@ bool launch_gemm(hmc_ctx* x, const GemmArgs& a_in, bool akm, bool bkm, cudaStrea
   if (tc) {
     x->launches++;
   } else {
+    if (pre && pre->only) {  // the SIMT engine would read a stale dense copy of these weights
+      x->err = std::string("tensor-core engine refused a '") + tag + "' GEMM of a planes-only layer";
+      throw Fail{HMC_E_STATE};
+    }
     launch_gemm_simt(x, a, akm, bkm, st);
   }
   const double flops = 2.0 * a.M * a.N * (double)a.K * a.batch;
@@ -384,7 +389,10 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
   if (L.bias) { a.bias = x->Wd + L.b_off; a.s_bias = x->P; }
   if (L.act == ACT_SIN) { a.D = L.D; a.ldd = L.n_out; a.sD = L.rows * L.n_out; }
   PreSplit pre;
-  if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc; }
+  if (L.tc_w) {
+    pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
+    pre.only = L.planes_only;
+  }
   launch_gemm(x, a, true, true, st, "fwd", L.tc_w ? &pre : nullptr);
 }
 
@@ -479,7 +487,10 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.epi = EPI_DACT; a.act = Pv.act;
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
       PreSplit pre;
-      if (L.tc_w) { pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc; }
+      if (L.tc_w) {
+        pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
+        pre.only = L.planes_only;
+      }
       float* cs_prev = ov ? N.cs[(i - 1) % 3] : N.colsum;
       if (Pv.bias_active && cs_prev) { a.colsum = cs_prev; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
       N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
@@ -1050,6 +1061,9 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         const bool mlp_out = (x->kind == HMC_MLP && i == (int)N.layers.size() - 1);
         if (mlp_out || L.n_in % 4 || L.n_out % 4 || L.n_in < 32 || L.n_out < 32) continue;
         L.tc_w = true;
+        // planes only when every GEMM reading these weights (forward, input gradient) takes the
+        // tensor-core path: not for sin layers (their forward runs on SIMT) nor short row counts
+        L.planes_only = L.act != ACT_SIN && N.rows >= 64 && !(getenv("HMC_DENSE_W") && atoi(getenv("HMC_DENSE_W")) == 1);
         L.q_off = x->Ptc;
         x->Ptc += (int64_t)L.n_in * L.n_out;
       }
@@ -1058,7 +1072,9 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (int64_t j = 0; j < x->k; ++j)
       for (auto& L : x->layers)
         if (L.tc_w && h_idx[j] >= L.w_off && h_idx[j] < L.w_off + (int64_t)L.n_in * L.n_out)
-          tcpos[j] = (int32_t)(L.q_off + (h_idx[j] - L.w_off));
+          // (planes-only entries encoded as -(q + 2), see put_param)
+          tcpos[j] = L.planes_only ? (int32_t)(-(L.q_off + (h_idx[j] - L.w_off)) - 2)
+                                   : (int32_t)(L.q_off + (h_idx[j] - L.w_off));
   }
   for (int ni = 0; ni < x->n_nets; ++ni) {
     NetInfo& N = x->nets[ni];
@@ -1138,7 +1154,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     // default: tf32 hi / lo planes written by the scatter (no B conversion in the GEMM);
     // HMC_TC_RAWB=1: one raw plane split in shared memory by the converters (half the L2
     // traffic, measured 2-3 % slower: the converters are on the critical path)
-    if (!getenv("HMC_TC_RAWB")) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    if (!(getenv("HMC_TC_RAWB") && atoi(getenv("HMC_TC_RAWB")) == 1)) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
     x->d_tcpos = dalloc<int32_t>(x, x->k, err);
     CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 4, cudaMemcpyHostToDevice));
     for (auto& L : x->layers)

@@ -45,19 +45,20 @@ struct KState {
 
 constexpr int KT = 256;  // threads of the per-chain state kernels
 
-// theta_j of chain c -> dense parameters (and the tf32 hi/lo planes of tensor-core layers)
+// theta_j of chain c -> dense parameters and/or the tf32 hi/lo planes of tensor-core layers:
+// tcpos[j] = -1: dense only; q >= 0: dense and planes at q; -(q + 2): planes only (layers whose
+// every weight-reading GEMM runs on the tensor cores: one scattered write fewer per step)
 __device__ __forceinline__ void put_param(const KState& s, int64_t c, int64_t j, float th) {
-  s.Wd[c * s.P + __ldg(s.idx + j)] = th;
-  if (s.tcpos) {
-    const int64_t q = __ldg(s.tcpos + j);
-    if (q >= 0) {
-      if (s.Wlo) {  // pre-split hi / lo planes
-        const float h = tf32_hi(th);
-        s.Whi[c * s.Ptc + q] = h;
-        s.Wlo[c * s.Ptc + q] = th - h;
-      } else {      // one raw plane (split in shared memory by the GEMM's converters)
-        s.Whi[c * s.Ptc + q] = th;
-      }
+  int64_t q = s.tcpos ? (int64_t)__ldg(s.tcpos + j) : -1;
+  if (q >= -1) s.Wd[c * s.P + __ldg(s.idx + j)] = th;
+  if (q < -1) q = -q - 2;
+  if (q >= 0) {
+    if (s.Wlo) {  // pre-split hi / lo planes
+      const float h = tf32_hi(th);
+      s.Whi[c * s.Ptc + q] = h;
+      s.Wlo[c * s.Ptc + q] = th - h;
+    } else {      // one raw plane (split in shared memory by the GEMM's converters)
+      s.Whi[c * s.Ptc + q] = th;
     }
   }
 }

@@ -1170,6 +1170,7 @@ struct PreSplit {
   const float* hi = nullptr;
   const float* lo = nullptr;
   int64_t ld = 0, stride = 0;
+  bool only = false;  // the planes are the only current copy of the weights (dense W not updated)
 };
 
 // Kernel instantiations: (A MN-major, B MN-major, B pre-split, epilogue) combinations the hot
