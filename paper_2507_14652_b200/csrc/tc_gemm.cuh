@@ -340,6 +340,8 @@ struct MnDesc {
   // plane written instead of two; |B - hi - lo| <= 2^-21 |B| as with the rna split
   int btrunc = 1;
   int pdl = 1;       // programmatic dependent launch (HMC_TC_PDL=0 disables)
+  int emit_lead = 1;  // emit steps end (1 + emit_lead) folds before the tile end; the act' / V
+                      // prefetch of the next tile follows one fold after the last store
   int tanh_end = 1;  // EPI_FWD tanh in registers at the tile end (1; +1 % with concurrent streams) or in emit steps (0)
   // mbarrier try_wait suspend-time hints (ns) of the producers / converters / epilogue waits: a
   // spinning waiter takes issue slots from the working warps of its SM sub-partition
@@ -872,7 +874,7 @@ __global__ void __launch_bounds__(NT, 1)
       int b, mt, nt;
       tile_of(t, b, mt, nt);
       const int rem = mt * n_nt + nt;  // tile index within the batch (residual partial slot)
-      bool prefetched = false;
+      bool prefetched = false, pf_due = false;
       if (loadx && pend == 0) {
         staging_free();
         issue_prefetch(b, mt, nt);
@@ -943,20 +945,24 @@ __global__ void __launch_bounds__(NT, 1)
         if (tla) atomicMax(&g_tctl[5][jc], clock64());  // last epilogue warp done
         if (te) g_tctl[18][jc] = clock64();
         if (ESPLIT) split_upto(jb + ESPLIT_D);  // B stages of K blocks < jb + ESPLIT_D
+        if (pf_due && !prefetched) {
+          // the last store of the parked tile was issued a fold ago: its read of the staging
+          // tiles has (mostly) completed, the next tile's act' / V tiles can be loaded in place
+          staging_free();
+          issue_prefetch(b, mt, nt);
+          prefetched = true;
+          pf_due = false;
+        }
         if (pend > 0) {
-          // the parked tile's steps spread evenly over this tile's folds, the last one a fold
-          // before the tile end (its store's read of the staging tile is done by the next park)
+          // the parked tile's steps spread evenly over the first folds of this tile, the last one
+          // (mn.emit_lead + 1) folds before the tile end
           const unsigned long long t_e0 = mn.prof ? clock64() : 0ull;
-          const int left = max(1, nch - 1 - c);
+          const int left = max(1, nch - 1 - mn.emit_lead - c);
           for (int todo = (pend + left - 1) / left; todo > 0 && pend > 0; --todo) {
             tstep = te; tstep_j = jc;
             emit_step(p_next++);
             tstep = false;
-            if (--pend == 0 && loadx && !prefetched) {
-              staging_free();
-              issue_prefetch(b, mt, nt);
-              prefetched = true;
-            }
+            if (--pend == 0 && loadx && !prefetched) pf_due = true;
           }
           if (mn.prof) pacc[2] += clock64() - t_e0;
         }
@@ -1231,6 +1237,7 @@ struct TcPlanner {
     if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
     if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
     if (const char* f = getenv("HMC_TC_TANHEND")) mn.tanh_end = atoi(f);
+    if (const char* f = getenv("HMC_TC_EMITLEAD")) mn.emit_lead = atoi(f);
     if (const char* f = getenv("HMC_TC_PDL")) mn.pdl = atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
     if (const char* f = getenv("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
