@@ -3,6 +3,11 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+# `make DEV=1`: developer build that reads the engine's tuning / profiling knobs (HMC_TC_*, ...)
+# from the environment (include/hmc.h "developer knobs"); the product build ignores them
+ifeq ($(DEV),1)
+FLAGS += -DHMC_DEV
+endif
 SRC := paper_2507_14652_b200/csrc/hmc.cu
 DEPS := $(wildcard paper_2507_14652_b200/csrc/*.cuh) include/hmc.h
 LIB := paper_2507_14652_b200/libhmc.so

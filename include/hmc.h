@@ -226,6 +226,21 @@ int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream);
 /* Name of the GEMM engine used for each layer GEMM class ("simt" or "tcgen05"). */
 const char* hmc_engine_info(const hmc_ctx* ctx);
 
+/* Divergence diagnostic ("gradient explosion"; reading Q5): counts[c] (host or
+ * device, uint32) = number of trajectories of chain c, since the context was created or last
+ * reset, whose proposal energy was non-finite or had |H* - H0| > 1000 (SPEC S:445's threshold).
+ * A flag only: such proposals are decided by the exact Metropolis test like any other (a
+ * non-finite H* always rejects).  reset != 0 zeroes the counters after reading.  Synchronises
+ * the context's stream.  HMC_E_CONFIG on NULL counts. */
+int hmc_divergences(hmc_ctx* ctx, uint32_t* counts, int32_t reset);
+
+/* Test hook: mode 1 makes contexts set up afterwards (process-wide) run every GEMM on the SIMT
+ * FP32 engine, 0 restores the automatic choice (tcgen05 wherever it takes the shape).  Returns
+ * HMC_E_CONFIG for any other mode.  Developer knobs of the tcgen05 engine (HMC_TC_* environment
+ * variables: barrier profiles, timelines, A/B toggles) are compiled in only with -DHMC_DEV
+ * (`make DEV=1`); the product library ignores the environment. */
+int hmc_debug_set_engine(int32_t mode);
+
 /* Live kernel timing.  hmc_profile(ctx, 1) makes the next trajectory graph capture CUDA event
  * nodes (cudaEventRecordExternal) around every kernel of the FIRST leapfrog step and around the
  * gradient-evaluation body of EVERY step; hmc_profile_read returns, for the most recently

@@ -38,24 +38,40 @@ def split_rhat(x):
     return float(np.sqrt(var_plus / W))
 
 
-def ess(x):
-    """x [C, S] draws of one scalar -> effective sample size (BDA3 11.8)."""
-    ps = split_chains(x)
+def autocorr(ps):
+    """rho_t, t = 0 .. n-1, of split chains ps [m, n] from the variogram (BDA3 11.7)."""
     m, n = ps.shape
     W, var_plus = _moments(ps)
     rho = [1.0]
     for t in range(1, n):
         V = np.sum((ps[:, t:] - ps[:, :-t]) ** 2) / (m * (n - t))
         rho.append(1.0 - V / (2.0 * var_plus))
-    rho = np.array(rho)
+    return np.array(rho)
+
+
+def truncated_sum(rho):
+    """sum_{t=1}^{T} rho_t with T the first ODD lag for which rho_{T+1} + rho_{T+2} < 0 (BDA3
+    11.8: "the first odd positive integer T"); when no odd lag qualifies the sum runs to the
+    last available lag n - 1.  Left-to-right order (the GPU kernel uses the same order)."""
+    n = len(rho)
     s = 0.0
     t = 1
     while t < n:
-        s += rho[t]
-        if t + 2 < n and rho[t + 1] + rho[t + 2] < 0:
+        s += rho[t]                       # rho_T for the odd candidate T = t
+        if t + 1 >= n:
             break
-        t += 1
-    return float(m * n / (1.0 + 2.0 * s))
+        if t + 2 < n and rho[t + 1] + rho[t + 2] < 0:
+            break                         # T = t (odd)
+        s += rho[t + 1]
+        t += 2
+    return s
+
+
+def ess(x):
+    """x [C, S] draws of one scalar -> effective sample size (BDA3 11.8)."""
+    ps = split_chains(x)
+    m, n = ps.shape
+    return float(m * n / (1.0 + 2.0 * truncated_sum(autocorr(ps))))
 
 
 def diagnostics(samples):

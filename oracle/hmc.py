@@ -119,6 +119,16 @@ def trajectory(target, theta, logp, grad, eps, L, it, chain):
             "theta_prop": th1, "p_prop": p1, "p0": p0, "H0": H0, "H1": H1, "u": u}
 
 
+# Divergence diagnostic ("gradient explosion"; SPEC S:445's |dH| > 1000
+# threshold, read as a flag only - Q5 keeps the exact Metropolis test as the sole decision).
+DIVERGENCE_DH = 1000.0
+
+
+def divergent(dH):
+    """A trajectory is divergent when its energy error is non-finite or |dH| > 1000."""
+    return bool(not math.isfinite(dH) or abs(dH) > DIVERGENCE_DH)
+
+
 def sample_chain(target, theta0, eps, L, iter0, S, chain):
     """S consecutive trajectories for one chain (P:234 while-loop); burn-in is the caller's."""
     theta = np.asarray(theta0, dtype=np.float64)

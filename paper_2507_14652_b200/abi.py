@@ -57,7 +57,7 @@ EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
            "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict",
-           "hmc_diagnostics", "hmc_partition"]
+           "hmc_diagnostics", "hmc_partition", "hmc_divergences", "hmc_debug_set_engine"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -107,17 +107,60 @@ def lib():
     return L
 
 
+_TORCH_DT = {np.dtype(np.float32): "torch.float32", np.dtype(np.float64): "torch.float64",
+             np.dtype(np.uint8): "torch.uint8", np.dtype(np.int32): "torch.int32",
+             np.dtype(np.uint32): "torch.uint32"}
+
+# (C, k) of the contexts created through this module, for the shape checks of _arg
+_CTX_SHAPE: dict = {}
+
+
 def _ptr(a, keep: list, dtype=None):
-    """Raw pointer of a torch tensor or NumPy array (None -> NULL)."""
+    """Raw pointer of an INPUT torch tensor or NumPy array (None -> NULL).  A NumPy input of
+    another dtype or layout is converted (a copy the library only reads); a torch tensor must
+    already have the dtype and be contiguous."""
+    return _arg(a, keep, dtype, out=False)
+
+
+def _arg(a, keep: list, dtype=None, count=None, out=True, name="array"):
+    """Raw pointer of an argument the library reads (out=False) or WRITES (out=True).  Written
+    arguments are never copied: a NumPy array or torch tensor of the wrong dtype, a
+    non-contiguous one, or one with the wrong element count raises (the library would otherwise
+    write past its end, or into a temporary copy the caller never sees)."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):          # torch.Tensor
-        assert a.is_contiguous(), "tensors must be contiguous"
+        if dtype is not None and str(a.dtype) != _TORCH_DT[np.dtype(dtype)]:
+            raise TypeError(f"{name}: torch dtype {a.dtype}, expected {_TORCH_DT[np.dtype(dtype)]}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name}: tensor must be contiguous")
+        if count is not None and a.numel() != count:
+            raise ValueError(f"{name}: {a.numel()} elements, expected {count}")
         keep.append(a)
         return a.data_ptr()
-    arr = np.ascontiguousarray(a, dtype=dtype) if dtype is not None else np.ascontiguousarray(a)
+    if out:
+        if not isinstance(a, np.ndarray):
+            raise TypeError(f"{name}: output arguments must be NumPy arrays or torch tensors")
+        if dtype is not None and a.dtype != np.dtype(dtype):
+            raise TypeError(f"{name}: dtype {a.dtype}, expected {np.dtype(dtype)}")
+        if not a.flags.c_contiguous or not a.flags.writeable:
+            raise ValueError(f"{name}: output array must be C-contiguous and writeable")
+        arr = a
+    else:
+        arr = np.ascontiguousarray(a, dtype=dtype) if dtype is not None else np.ascontiguousarray(a)
+    if count is not None and arr.size != count:
+        raise ValueError(f"{name}: {arr.size} elements, expected {count}")
     keep.append(arr)
     return arr.ctypes.data
+
+
+def _shape(ctx):
+    """(C, k) of a context made by this module (None, None for a foreign handle)."""
+    return _CTX_SHAPE.get(ctx, (None, None))
+
+
+def _n(*dims):
+    return None if any(d is None for d in dims) else int(np.prod(dims))
 
 
 def _check(rc, ctx=None):
@@ -163,8 +206,10 @@ def hmc_setup(arch: hmc_arch, data: hmc_data, cfg: hmc_config, stream=None) -> i
 
 def hmc_grad(ctx, theta, logp, grad, stream=None):
     keep = []
-    _check(lib().hmc_grad(ctx, _ptr(theta, keep, np.float32), _ptr(logp, keep),
-                          _ptr(grad, keep), _stream(stream)), ctx)
+    C, k = _shape(ctx)
+    _check(lib().hmc_grad(ctx, _arg(theta, keep, np.float32, _n(C, k), out=False, name="theta"),
+                          _arg(logp, keep, np.float64, C, name="logp"),
+                          _arg(grad, keep, np.float32, _n(C, k), name="grad"), _stream(stream)), ctx)
 
 
 def hmc_logpost_const(ctx) -> float:
@@ -173,18 +218,30 @@ def hmc_logpost_const(ctx) -> float:
     return c.value
 
 
+def _state_args(ctx, theta, logp, grad, keep):
+    """theta [C x k] f32, logp [C] f64, grad [C x k] f32: in/out chain state (never copied)."""
+    C, k = _shape(ctx)
+    return (_arg(theta, keep, np.float32, _n(C, k), name="theta"), _arg(logp, keep, np.float64, C, name="logp"),
+            _arg(grad, keep, np.float32, _n(C, k), name="grad"))
+
+
 def hmc_trajectory(ctx, theta, logp, grad, eps, L, it, acc=None, dH=None, stream=None):
     keep = []
-    _check(lib().hmc_trajectory(ctx, _ptr(theta, keep), _ptr(logp, keep), _ptr(grad, keep),
-                                float(eps), int(L), int(it), _ptr(acc, keep), _ptr(dH, keep),
-                                _stream(stream)), ctx)
+    C, _ = _shape(ctx)
+    th, lp, g = _state_args(ctx, theta, logp, grad, keep)
+    _check(lib().hmc_trajectory(ctx, th, lp, g, float(eps), int(L), int(it),
+                                _arg(acc, keep, np.uint8, C, name="acc"),
+                                _arg(dH, keep, np.float64, C, name="dH"), _stream(stream)), ctx)
 
 
 def hmc_sample(ctx, theta, logp, grad, eps, L, iter0, S, samples, acc=None, dH=None, stream=None):
     keep = []
-    _check(lib().hmc_sample(ctx, _ptr(theta, keep), _ptr(logp, keep), _ptr(grad, keep), float(eps),
-                            int(L), int(iter0), int(S), _ptr(samples, keep), _ptr(acc, keep),
-                            _ptr(dH, keep), _stream(stream)), ctx)
+    C, k = _shape(ctx)
+    th, lp, g = _state_args(ctx, theta, logp, grad, keep)
+    _check(lib().hmc_sample(ctx, th, lp, g, float(eps), int(L), int(iter0), int(S),
+                            _arg(samples, keep, np.float32, _n(C, S, k), name="samples"),
+                            _arg(acc, keep, np.uint8, _n(C, S), name="acc"),
+                            _arg(dH, keep, np.float64, _n(C, S), name="dH"), _stream(stream)), ctx)
 
 
 def hmc_destroy(ctx):
@@ -206,7 +263,28 @@ def hmc_philox_words(seed, tag, it, chain, nblocks, out, stream=None):
 
 def hmc_momentum(ctx, it, out, stream=None):
     keep = []
-    _check(lib().hmc_momentum(ctx, int(it), _ptr(out, keep), _stream(stream)), ctx)
+    C, k = _shape(ctx)
+    _check(lib().hmc_momentum(ctx, int(it), _arg(out, keep, np.float32, _n(C, k), name="p"), _stream(stream)), ctx)
+
+
+def hmc_divergences(ctx, reset: bool = False):
+    """Per-chain counts of divergent trajectories (non-finite or |dH| > 1000) since creation or the
+    last reset (include/hmc.h hmc_divergences); a uint32 NumPy array [C]."""
+    C, _ = _shape(ctx)
+    if C is None:
+        raise ValueError("hmc_divergences needs a context created through abi.Context")
+    out = np.zeros(C, dtype=np.uint32)
+    L = lib()
+    L.hmc_divergences.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+    _check(L.hmc_divergences(ctx, out.ctypes.data, int(bool(reset))), ctx)
+    return out
+
+
+def hmc_debug_set_engine(mode: int):
+    """Test hook: 1 = contexts set up afterwards run every GEMM on the SIMT engine; 0 = automatic."""
+    L = lib()
+    L.hmc_debug_set_engine.argtypes = [ctypes.c_int32]
+    _check(L.hmc_debug_set_engine(int(mode)))
 
 
 def hmc_engine_info(ctx) -> str:
@@ -268,9 +346,10 @@ def hmc_adapt(ctx, theta, logp, grad, eps0, L, iter0, n_adapt, delta, acc=None, 
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     C = int(theta.shape[0])
     out = np.empty(C, dtype=np.float64)
-    _check(L_.hmc_adapt(ctx, _ptr(theta, keep, np.float32), _ptr(logp, keep, np.float64), _ptr(grad, keep, np.float32),
-                        float(eps0), int(L), int(iter0), int(n_adapt), float(delta), out.ctypes.data,
-                        _ptr(acc, keep, np.uint8), _ptr(dH, keep, np.float64), _stream(stream)), ctx)
+    th, lp, g = _state_args(ctx, theta, logp, grad, keep)
+    _check(L_.hmc_adapt(ctx, th, lp, g, float(eps0), int(L), int(iter0), int(n_adapt), float(delta), out.ctypes.data,
+                        _arg(acc, keep, np.uint8, C * int(n_adapt), name="acc"),
+                        _arg(dH, keep, np.float64, C * int(n_adapt), name="dH"), _stream(stream)), ctx)
     return out
 
 
@@ -400,10 +479,12 @@ class Context:
             c.nccl_id = ctypes.addressof(idbuf)
         self.ctx = hmc_setup(a, d, c)
         self.C, self.k, self.P = C, c.k, c.P
+        _CTX_SHAPE[self.ctx] = (C, int(c.k))
         self._n_out = int(d.n) if arch.kind == "mlp" else int(d.n_c * d.n_x)
 
     def close(self):
         if self.ctx:
+            _CTX_SHAPE.pop(self.ctx, None)
             hmc_destroy(self.ctx)
             self.ctx = None
 

@@ -119,9 +119,17 @@ struct hmc_ctx {
   float* R = nullptr;
   int sq = 0;                    // sensitivity mode (hmc_sensitivity): squared weight-gradient sums
   int colred_chunks = 0;
-  double* d_eps = nullptr;   // [C] per-chain step sizes
+  double* d_eps = nullptr;   // [C] per-chain step sizes the trajectory graph reads
+  double* d_epsbar = nullptr;  // [C] per-chain averaged steps of the last hmc_adapt (eps == 0 uses them)
   double* d_da = nullptr;    // [C x 4] dual-averaging state (NEXT-2)
-  bool adapted = false;      // per-chain epsbar from hmc_adapt in d_eps
+  bool adapted = false;      // d_epsbar holds hmc_adapt's result
+  uint32_t* d_div = nullptr;  // [C] divergent-trajectory counters (hmc_divergences)
+  // grow-only device staging of host output buffers (hmc_sample / hmc_adapt with host pointers);
+  // every call that stages synchronises before returning, so a buffer is free at the next call
+  struct Stage {
+    void* p = nullptr;
+    size_t cap = 0;
+  } stage_samples, stage_acc, stage_dH, stage_eps;
   Rec* d_rec = nullptr;
   uint8_t* tmp_acc = nullptr;
   double* tmp_dH = nullptr;
@@ -167,11 +175,13 @@ struct hmc_ctx {
     s.Wd = Wd; s.Whi = Whi; s.Wlo = Wlo; s.tcpos = d_tcpos; s.Ptc = Ptc; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
     s.wrk_theta = wrk_theta; s.wrk_grad = wrk_grad; s.wrk_logp = wrk_logp; s.p = p; s.H0 = H0;
     s.gl = gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
-    s.eps = d_eps; s.da = d_da; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
+    s.eps = d_eps; s.da = d_da; s.div = d_div; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
     return s;
   }
   ~hmc_ctx() {
     prof_clear();
+    for (Stage* g : {&stage_samples, &stage_acc, &stage_dH, &stage_eps})
+      if (g->p) cudaFree(g->p);
     if (grad_exec) cudaGraphExecDestroy(grad_exec);
     if (traj_exec) cudaGraphExecDestroy(traj_exec);
     if (comm) ncclCommDestroy(comm);
@@ -304,15 +314,26 @@ void prof_end(hmc_ctx* x, int id, cudaStream_t st, const std::string& name, doub
   r.bytes = bytes;
 }
 
+// a GEMM the tensor-core engine accepted must launch there: a failure is an error (HMC_E_CUDA),
+// never a silent re-run on the SIMT engine
+void tc_launch_or_throw(hmc_ctx* x, const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const char* tag,
+                        const PreSplit* pre = nullptr) {
+  const cudaError_t e = x->tc.launch(a, akm, bkm, st, pre);
+  if (e != cudaSuccess) {
+    x->err = std::string("tcgen05 '") + tag + "' GEMM launch failed: " + cudaGetErrorString(e);
+    throw Fail{HMC_E_CUDA};
+  }
+}
+
 // returns true if the tensor-core engine ran it
 bool launch_gemm(hmc_ctx* x, const GemmArgs& a_in, bool akm, bool bkm, cudaStream_t st, const char* tag,
                  const PreSplit* pre = nullptr) {
   GemmArgs a = a_in;
   a.sq = x->sq;
   const int id = prof_begin(x, st);
-  bool tc = x->tc.accepts(a, akm, bkm, pre);
-  if (tc) tc = x->tc.launch(a, akm, bkm, st, pre);
+  const bool tc = x->tc.accepts(a, akm, bkm, pre);
   if (tc) {
+    tc_launch_or_throw(x, a, akm, bkm, st, tag, pre);
     x->launches++;
   } else {
     if (pre && pre->only) {  // the SIMT engine would read a stale dense copy of these weights
@@ -430,16 +451,16 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
       if (L.ksplit > 1 && N.gl_part) { a.ksplit = L.ksplit; a.gl_part = N.gl_part; }
-      static const bool fuse_bias = !(getenv("HMC_BIAS_FUSE") && atoi(getenv("HMC_BIAS_FUSE")) == 0);
+      static const bool fuse_bias = !(dev_env("HMC_BIAS_FUSE") && atoi(dev_env("HMC_BIAS_FUSE")) == 0);
       const bool bias_in_gemm = fuse_bias && L.bias_active && N.cs_ready;  // (tcgen05 path only)
       if (bias_in_gemm) {
         a.bcs_nblk = (int)((L.rows + 31) / 32);
         a.bcs = cs_i; a.s_bcs = (int64_t)a.bcs_nblk * L.n_out; a.bcs_slot = x->d_slot + L.b_off;
       }
       const int id = prof_begin(x, st);
-      bool tc = x->tc.accepts(a, false, false);
-      if (tc) tc = x->tc.launch(a, false, false, st);
+      const bool tc = x->tc.accepts(a, false, false);
       if (tc) {
+        tc_launch_or_throw(x, a, false, false, st, "wgrad");
         x->launches++;
         if (a.ksplit > 1) {  // fixed-order sum of the splits' partial k-vector entries
           k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.ws_hi - L.ws_lo + 255) / 256, 256)), x->C),
@@ -917,6 +938,7 @@ void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, in
   x->h_rec->delta = delta;
   CK(cudaMemcpyAsync(x->d_rec, x->h_rec, sizeof(Rec), cudaMemcpyHostToDevice, x->st));
   if (eps > 0) k_fill_d<<<1, 256, 0, x->st>>>(x->d_eps, x->C, eps);
+  else if (!adapt) CK(cudaMemcpyAsync(x->d_eps, x->d_epsbar, (size_t)x->C * 8, cudaMemcpyDeviceToDevice, x->st));
   CK(cudaEventRecord(x->ev_stage, x->st));
 }
 
@@ -992,8 +1014,9 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   x->mode = cfg->mode;
   x->rank = cfg->rank;
   x->world = cfg->world;
-  CFG(x->world >= 1 && x->rank >= 0 && x->rank < x->world, "need 0 <= rank < world");
-  CFG(x->mode == HMC_MODE_DATA || x->world >= 1, "world");
+  CFG(x->world == 1 || x->world == 2 || x->world == 4 || x->world == 8, "world must be 1, 2, 4 or 8 (one node)");
+  CFG(x->rank >= 0 && x->rank < x->world, "need 0 <= rank < world");
+  CFG(x->mode != HMC_MODE_SINGLE || x->world == 1, "SINGLE mode needs world == 1 (DATA or CHAIN for world > 1)");
   // ---- data ----
   std::vector<float> hx, hy, hu, hq, hv;
   if (x->kind == HMC_MLP) {
@@ -1005,7 +1028,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (float v : hx) CFG(std::isfinite(v), "x must be finite");
     for (float v : hy) CFG(std::isfinite(v), "y must be finite");
     x->nets[0].rows = x->n;
-    const char* e = getenv("HMC_STREAMS");
+    const char* e = dev_env("HMC_STREAMS");
     x->wgrad_ov = !(e && atoi(e) == 1);
   } else {
     CFG(data->u && data->q && data->v && data->n_c >= 1 && data->n_x >= 1, "DeepONet data needs u, q, v, n_c, n_x >= 1");
@@ -1022,7 +1045,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     }
     x->n_c_loc = x->xb ? x->n_c / cfg->world : x->n_c;
     {
-      const char* e = getenv("HMC_STREAMS");
+      const char* e = dev_env("HMC_STREAMS");
       x->two_streams = !x->unaligned && !x->xb && !(e && atoi(e) == 1);
       x->wgrad_ov = x->two_streams;
     }
@@ -1037,8 +1060,13 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->nets[1].rows = q_rows;
   }
   const int64_t n_local = x->kind == HMC_MLP ? x->n : x->n_c * x->n_x;
-  x->n_global = data->n_global > 0 ? data->n_global : n_local;
+  x->n_global = data->n_global > 0 ? data->n_global : (x->mode == HMC_MODE_DATA ? n_local * x->world : n_local);
   if (x->mode != HMC_MODE_DATA || x->world == 1) CFG(x->n_global == n_local, "n_global must equal the local size outside DATA mode");
+  // DATA mode: equal shards (SURVEY §8(b) validation): every rank holds n_global / world data
+  // points (ROWS: a row block; POINTS_XB: all n_c conditions x n_x / world points)
+  if (x->mode == HMC_MODE_DATA)
+    CFG(n_local * x->world == x->n_global, ("DATA mode needs equal shards: local size " + std::to_string(n_local) + " x world " +
+                                            std::to_string(x->world) + " != n_global " + std::to_string(x->n_global)).c_str());
   // ---- slot map, per-layer activity, l_min ----
   std::vector<int32_t> slot((size_t)x->P, -1);
   for (int64_t j = 0; j < x->k; ++j) slot[h_idx[j]] = (int32_t)j;
@@ -1063,7 +1091,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         L.tc_w = true;
         // planes only when every GEMM reading these weights (forward, input gradient) takes the
         // tensor-core path: not for sin layers (their forward runs on SIMT) nor short row counts
-        L.planes_only = L.act != ACT_SIN && N.rows >= 64 && !(getenv("HMC_DENSE_W") && atoi(getenv("HMC_DENSE_W")) == 1);
+        L.planes_only = L.act != ACT_SIN && N.rows >= 64 && !(dev_env("HMC_DENSE_W") && atoi(dev_env("HMC_DENSE_W")) == 1);
         L.q_off = x->Ptc;
         x->Ptc += (int64_t)L.n_in * L.n_out;
       }
@@ -1154,7 +1182,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     // default: tf32 hi / lo planes written by the scatter (no B conversion in the GEMM);
     // HMC_TC_RAWB=1: one raw plane split in shared memory by the converters (half the L2
     // traffic, measured 2-3 % slower: the converters are on the critical path)
-    if (!(getenv("HMC_TC_RAWB") && atoi(getenv("HMC_TC_RAWB")) == 1)) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
+    if (!(dev_env("HMC_TC_RAWB") && atoi(dev_env("HMC_TC_RAWB")) == 1)) x->Wlo = dalloc<float>(x, (size_t)C * x->Ptc, err);
     x->d_tcpos = dalloc<int32_t>(x, x->k, err);
     CK(cudaMemcpy(x->d_tcpos, tcpos.data(), x->k * 4, cudaMemcpyHostToDevice));
     for (auto& L : x->layers)
@@ -1175,6 +1203,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   x->H0 = dalloc<double>(x, C, err);
   x->lik = dalloc<double>(x, C, err);
   x->d_eps = dalloc<double>(x, C, err);
+  x->d_epsbar = dalloc<double>(x, C, err);
+  x->d_div = dalloc<uint32_t>(x, C, err);
   x->d_da = dalloc<double>(x, (size_t)4 * C, err);
   x->d_rec = dalloc<Rec>(x, 1, err);
   x->tmp_acc = dalloc<uint8_t>(x, C, err);
@@ -1396,24 +1426,27 @@ static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, doubl
   float* d_samples = nullptr;
   uint8_t* d_acc = nullptr;
   double* d_dH = nullptr;
-  DevBuf tmp;
-  auto tmp_alloc = [&](size_t bytes) -> void* {
-    void* p = nullptr;
-    CK(cudaMalloc(&p, bytes));
-    tmp.ptrs.push_back(p);
-    return p;
+  auto stage = [&](hmc_ctx::Stage& g, size_t bytes) -> void* {
+    if (bytes > g.cap) {
+      if (g.p) CK(cudaFree(g.p));
+      g.p = nullptr;
+      g.cap = 0;
+      CK(cudaMalloc(&g.p, bytes));
+      g.cap = bytes;
+    }
+    return g.p;
   };
   if (samples) {
     if (is_device_ptr(samples)) d_samples = samples;
-    else { host = true; d_samples = (float*)tmp_alloc(Ck * S * 4); }
+    else { host = true; d_samples = (float*)stage(ctx->stage_samples, Ck * S * 4); }
   }
   if (acc) {
     if (is_device_ptr(acc)) d_acc = acc;
-    else { host = true; d_acc = (S == 1) ? ctx->tmp_acc : (uint8_t*)tmp_alloc((size_t)ctx->C * S); }
+    else { host = true; d_acc = (S == 1) ? ctx->tmp_acc : (uint8_t*)stage(ctx->stage_acc, (size_t)ctx->C * S); }
   }
   if (dH) {
     if (is_device_ptr(dH)) d_dH = dH;
-    else { host = true; d_dH = (S == 1) ? ctx->tmp_dH : (double*)tmp_alloc((size_t)ctx->C * S * 8); }
+    else { host = true; d_dH = (S == 1) ? ctx->tmp_dH : (double*)stage(ctx->stage_dH, (size_t)ctx->C * S * 8); }
   }
   build_traj_graph(ctx, L, err);
   sync_in(ctx, us, err);
@@ -1427,10 +1460,9 @@ static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, doubl
     set_rec(ctx, d_samples, d_acc, d_dH, S, iter0, eps, err);
   }
   for (int s = 0; s < S; ++s) CK(cudaGraphLaunch(ctx->traj_exec, ctx->st));
-  if (adapt) {
-    double* d_out = (double*)tmp_alloc((size_t)ctx->C * 8);
-    k_da_finish<<<1, 256, 0, ctx->st>>>(ctx->d_eps, ctx->d_da, ctx->C, d_out);
-    CK(cudaMemcpyAsync(eps_bar, d_out, (size_t)ctx->C * 8, cudaMemcpyDefault, ctx->st));
+  if (adapt) {  // the averaged steps: kept in the context (eps == 0 later) and copied out
+    k_da_finish<<<1, 256, 0, ctx->st>>>(ctx->d_eps, ctx->d_da, ctx->C, ctx->d_epsbar);
+    CK(cudaMemcpyAsync(eps_bar, ctx->d_epsbar, (size_t)ctx->C * 8, cudaMemcpyDefault, ctx->st));
     host = true;
     ctx->adapted = true;
   }
@@ -1440,7 +1472,7 @@ static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, doubl
   if (samples && d_samples != samples) cpy(samples, d_samples, Ck * S * 4, ctx->st, err);
   if (acc && d_acc != acc) cpy(acc, d_acc, (size_t)ctx->C * S, ctx->st, err);
   if (dH && d_dH != dH) cpy(dH, d_dH, (size_t)ctx->C * S * 8, ctx->st, err);
-  sync_out(ctx, us, host || !tmp.ptrs.empty(), err);
+  sync_out(ctx, us, host, err);
   API_END
 }
 
@@ -1752,6 +1784,24 @@ int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream) {
 
 const char* hmc_engine_info(const hmc_ctx* ctx) { return ctx ? ctx->engine.c_str() : ""; }
 
+int hmc_debug_set_engine(int32_t mode) {
+  if (mode != 0 && mode != 1) {
+    g_err = "config: engine mode must be 0 (automatic) or 1 (SIMT only)";
+    return HMC_E_CONFIG;
+  }
+  engine_override() = mode;
+  return HMC_OK;
+}
+
+int hmc_divergences(hmc_ctx* ctx, uint32_t* counts, int32_t reset) {
+  API_BEGIN(ctx)
+  CFG(counts, "counts must be non-NULL");
+  CK(cudaStreamSynchronize(ctx->st));
+  CK(cudaMemcpy(counts, ctx->d_div, (size_t)ctx->C * 4, cudaMemcpyDefault));
+  if (reset) CK(cudaMemset(ctx->d_div, 0, (size_t)ctx->C * 4));
+  API_END
+}
+
 int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M, int32_t N, int32_t K,
                    int32_t batch, const float* A, int64_t lda, int64_t sA, const float* B, int64_t ldb, int64_t sB,
                    float* C, int64_t ldc, int64_t sC, void* stream) {
@@ -1765,9 +1815,14 @@ int hmc_debug_gemm(int32_t engine, int32_t a_kmajor, int32_t b_kmajor, int32_t M
   a.A = A; a.lda = lda; a.sA = sA; a.B = B; a.ldb = ldb; a.sB = sB; a.C = C; a.ldc = ldc; a.sC = sC;
   cudaStream_t st = (cudaStream_t)stream;
   if (engine == 1) {
-    if (!tcp.accepts(a, a_kmajor != 0, b_kmajor != 0) || !tcp.launch(a, a_kmajor != 0, b_kmajor != 0, st)) {
+    if (!tcp.accepts(a, a_kmajor != 0, b_kmajor != 0)) {
       g_err = "tcgen05 engine does not take this GEMM";
       return HMC_E_CONFIG;
+    }
+    const cudaError_t e = tcp.launch(a, a_kmajor != 0, b_kmajor != 0, st);
+    if (e != cudaSuccess) {
+      g_err = std::string("tcgen05 launch failed: ") + cudaGetErrorString(e);
+      return HMC_E_CUDA;
     }
   } else {
     hmc_ctx dummy;

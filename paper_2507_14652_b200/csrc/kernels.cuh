@@ -7,6 +7,10 @@
 namespace hmc {
 
 // Device-side record of hmc_sample progress (written by k_mh / k_advance inside the graph).
+// |H* - H0| above which a trajectory counts as divergent (SPEC S:445's threshold, kept as a
+// diagnostic only: Q5)
+constexpr double DIVERGENCE_DH = 1000.0;
+
 struct Rec {
   float* samples;   // [C x S x k] or nullptr
   uint8_t* acc;     // [C x S] or nullptr
@@ -39,6 +43,7 @@ struct KState {
   double inv_sp2;              // 1 / sigma_p^2
   double* eps;                 // [C] per-chain step sizes (device)
   double* da;                  // [C x 4] dual-averaging state: mu, Hbar, log epsbar, m
+  uint32_t* div;               // [C] divergent trajectories (non-finite or |dH| > 1000) since reset
   Rec* rec;
   uint32_t key0, key1;
 };
@@ -409,19 +414,22 @@ __global__ void __launch_bounds__(DIAG_T) k_diag(const float* __restrict__ x, in
       __syncthreads();
       return r;
     };
+    // truncation (BDA3 11.8): sum rho_1 .. rho_T, T the first ODD lag with rho_{T+1} + rho_{T+2}
+    // < 0 (all available lags when none qualifies); left-to-right like the oracle
     double ssum = 0.0;
-    double r1 = n > 1 ? rho(1) : 0.0, r2 = n > 2 ? rho(2) : 0.0;
-    for (int64_t t = 1; t < n; ++t) {
-      // invariant: r1 = rho_t, r2 = rho_{t+1} (when t + 1 < n)
-      ssum += r1;
+    double rt = n > 1 ? rho(1) : 0.0;  // rho_t of the odd candidate t
+    for (int64_t t = 1; t < n; t += 2) {
+      ssum += rt;
+      if (t + 1 >= n) break;
+      const double ra = rho(t + 1);
       if (t + 2 < n) {
-        const double r3 = rho(t + 2);
-        if (r2 + r3 < 0.0) break;
-        r1 = r2;
-        r2 = r3;
+        const double rb = rho(t + 2);
+        if (ra + rb < 0.0) break;  // T = t
+        ssum += ra;
+        rt = rb;
       } else {
-        r1 = r2;
-        r2 = 0.0;
+        ssum += ra;
+        break;
       }
     }
     if (threadIdx.x == 0) ess[j] = (double)m * (double)n / (1.0 + 2.0 * ssum);
@@ -648,6 +656,9 @@ __global__ void __launch_bounds__(KT) k_mh(KState s) {
     if (acc) s.cur_logp[c] = s.wrk_logp[c];
     if (rec->acc) rec->acc[(int64_t)c * rec->S + sidx] = (uint8_t)acc;
     if (rec->dH) rec->dH[(int64_t)c * rec->S + sidx] = H1 - H0;
+    // divergence diagnostic ("gradient explosion" P:488; Q5): flagged, never a
+    // rejection rule of its own (the exact test above decides)
+    if (!isfinite(H1) || fabs(H1 - H0) > DIVERGENCE_DH) s.div[c] += 1u;
     if (rec->adapt) {
       // dual averaging (Hoffman & Gelman Algorithm 5; DESIGN.md NEXT-2): gamma 0.05,
       // t0 10, kappa 0.75; alpha = min(1, exp(H0 - H*)), 0 for a non-finite H*
@@ -692,10 +703,7 @@ __global__ void k_da_init(double* __restrict__ eps, double* __restrict__ da, int
   }
 }
 __global__ void k_da_finish(double* __restrict__ eps, const double* __restrict__ da, int C, double* __restrict__ out) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
-    eps[c] = exp(da[4 * c + 2]);
-    out[c] = eps[c];
-  }
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) out[c] = exp(da[4 * c + 2]);
 }
 __global__ void k_fill_d(double* __restrict__ p, int n, double v) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) p[c] = v;

@@ -1211,6 +1211,23 @@ inline const TcVariant* tc_variants(int* n) {
   return v;
 }
 
+// Developer knobs (timelines, barrier profiles, A/B toggles of the engine) are read from the
+// environment only in a -DHMC_DEV build (`make DEV=1`); the product library ignores them.
+inline const char* dev_env(const char* name) {
+#ifdef HMC_DEV
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+// Process-wide engine override set through hmc_debug_set_engine (tests): 0 = automatic
+// (tcgen05 where it takes the shape, SIMT otherwise), 1 = SIMT only.  Read at hmc_setup.
+inline int& engine_override() {
+  static int v = 0;
+  return v;
+}
+
 struct TcPlanner {
   bool enabled = false;
   int num_sms = 148;
@@ -1221,8 +1238,7 @@ struct TcPlanner {
 
   void init() {
     enabled = false;
-    const char* eng = getenv("HMC_ENGINE");
-    if (eng && strcmp(eng, "simt") == 0) return;
+    if (engine_override() == 1) return;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return;
     cudaDeviceProp p;
@@ -1233,15 +1249,15 @@ struct TcPlanner {
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
     encode = (tc::EncodeTiledFn)fn;
-    if (const char* f = getenv("HMC_TC_PROF")) mn.prof = atoi(f);
-    if (const char* f = getenv("HMC_TC_DBG")) mn.dbg = atoi(f);
-    if (const char* f = getenv("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
-    if (const char* f = getenv("HMC_TC_TANHEND")) mn.tanh_end = atoi(f);
-    if (const char* f = getenv("HMC_TC_EMITLEAD")) mn.emit_lead = atoi(f);
-    if (const char* f = getenv("HMC_TC_PDL")) mn.pdl = atoi(f);
-    if (const char* f = getenv("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
-    if (const char* f = getenv("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
-    if (const char* f = getenv("HMC_TC_HINT_E")) mn.hint_e = (uint32_t)atoi(f);
+    if (const char* f = dev_env("HMC_TC_PROF")) mn.prof = atoi(f);
+    if (const char* f = dev_env("HMC_TC_DBG")) mn.dbg = atoi(f);
+    if (const char* f = dev_env("HMC_TC_BTRUNC")) mn.btrunc = atoi(f);
+    if (const char* f = dev_env("HMC_TC_TANHEND")) mn.tanh_end = atoi(f);
+    if (const char* f = dev_env("HMC_TC_EMITLEAD")) mn.emit_lead = atoi(f);
+    if (const char* f = dev_env("HMC_TC_PDL")) mn.pdl = atoi(f);
+    if (const char* f = dev_env("HMC_TC_HINT_P")) mn.hint_p = (uint32_t)atoi(f);
+    if (const char* f = dev_env("HMC_TC_HINT_C")) mn.hint_c = (uint32_t)atoi(f);
+    if (const char* f = dev_env("HMC_TC_HINT_E")) mn.hint_e = (uint32_t)atoi(f);
     static bool attr_done = false;
     if (!attr_done) {
       int n = 0;
@@ -1340,8 +1356,10 @@ struct TcPlanner {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
 
-  // Returns false if a tensor map could not be encoded (caller falls back to SIMT).
-  bool launch(const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const PreSplit* pre = nullptr) const {
+  // Launches a GEMM accepts() took.  Returns cudaSuccess, or the error: a tensor map that could
+  // not be encoded (cudaErrorInvalidValue) or the launch's own error.  Callers report it
+  // (HMC_E_CUDA); there is no silent fallback to the SIMT engine.
+  cudaError_t launch(const GemmArgs& a, bool akm, bool bkm, cudaStream_t st, const PreSplit* pre = nullptr) const {
     if (pre && !pre->lo) {  // raw weight plane: an ordinary B operand
       GemmArgs b = a;
       b.B = pre->hi; b.ldb = pre->ld; b.sB = pre->stride;
@@ -1349,7 +1367,7 @@ struct TcPlanner {
     }
     const bool amn = !akm, bmn = !bkm;
     const TcVariant* v = find(amn, bmn, pre != nullptr, a.epi);
-    if (!v) return false;
+    if (!v) return cudaErrorInvalidValue;
     CUtensorMap mA, mB, mB2, mC, mX;
     memset(&mB2, 0, sizeof(mB2));
     memset(&mC, 0, sizeof(mC));
@@ -1373,7 +1391,7 @@ struct TcPlanner {
     if (a.epi == EPI_DACT && a.act != ACT_ID)
       ok = ok && map_store(&mX, const_cast<float*>(a.dsrc), a.M, a.N, a.ld_dsrc, a.s_dsrc, a.batch);
     if (a.epi == EPI_RESID) ok = ok && map_store(&mX, const_cast<float*>(a.V), a.M, a.N, a.ldv, 0, 1);
-    if (!ok) return false;
+    if (!ok) return cudaErrorInvalidValue;
     const int pairs = (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch *
                       ((a.epi == EPI_WGRAD && a.ksplit > 1) ? a.ksplit : 1);
     const int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
@@ -1395,8 +1413,7 @@ struct TcPlanner {
     attr[1].val.programmaticStreamSerializationAllowed = mn.pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    if (cudaLaunchKernelEx(&cfg, v->fn, mA, mB, mB2, mC, mX, a, md) != cudaSuccess) return false;
-    return true;
+    return cudaLaunchKernelEx(&cfg, v->fn, mA, mB, mB2, mC, mX, a, md);
   }
 };
 

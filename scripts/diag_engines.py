@@ -17,8 +17,7 @@ for cfg in cfgs:
     lr, gr = t.logp_grad(th[1])
     ent = layout_entries(prob.arch)
     for eng in ["simt", "tc"]:
-        if eng == "simt": os.environ["HMC_ENGINE"] = "simt"
-        else: os.environ.pop("HMC_ENGINE", None)
+        abi.hmc_debug_set_engine(1 if eng == "simt" else 0)
         with abi.Context(prob) as c:
             info = abi.hmc_engine_info(c.ctx)
             lp, g = gpu_grad(c, th)

@@ -55,3 +55,35 @@ def test_diagnostics_of_gpu_samples_blr():
     np.testing.assert_allclose(rh, rr, rtol=1e-9)
     np.testing.assert_allclose(es, er, rtol=1e-8)
     assert np.all(rh < 1.05) and np.all(es > 100)
+
+
+def _every_lag_sum(rho):
+    """The rule BDA3 does NOT use (stop after ANY lag t with rho_{t+1} + rho_{t+2} < 0); only to
+    make sure the draws below separate it from the odd-lag rule."""
+    s, n = 0.0, len(rho)
+    for t in range(1, n):
+        s += rho[t]
+        if t + 2 < n and rho[t + 1] + rho[t + 2] < 0:
+            break
+    return s
+
+
+def test_ess_odd_lag_truncation_on_gpu():
+    """Short iid chains, whose autocorrelations flip sign at random lags: for many parameters the
+    first negative pair follows an even lag, where the odd-lag rule (BDA3 11.8) and an every-lag
+    rule give different ESS.  The GPU must follow the odd-lag rule (the oracle)."""
+    torch_cuda()
+    from paper_2507_14652_b200 import abi
+    g = np.random.default_rng(77)
+    C, S, k = 2, 24, 200
+    x = g.normal(size=(C, S, k)).astype(np.float32)
+    rh, es = abi.hmc_diagnostics(x)
+    rr, er = od.diagnostics(x.astype(np.float64))
+    np.testing.assert_allclose(es, er, rtol=1e-9)
+    np.testing.assert_allclose(rh, rr, rtol=1e-10)
+    differ = 0
+    for j in range(k):
+        ps = od.split_chains(x[:, :, j].astype(np.float64))
+        rho = od.autocorr(ps)
+        differ += int(abs(_every_lag_sum(rho) - od.truncated_sum(rho)) > 1e-12)
+    assert differ >= 10, differ

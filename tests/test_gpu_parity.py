@@ -63,10 +63,15 @@ TINY = {
 }
 
 
+# fixed per-case seeds (reproducible across processes, unlike salted str hashes)
+TINY_SEED = {"mlp_ragged": 21, "mlp_sin_nobias": 22, "mlp_deep_narrow": 23, "deeponet_ragged": 24,
+             "deeponet_sin": 25}
+
+
 @pytest.mark.parametrize("name", sorted(TINY))
 def test_grad_tiny(name):
     arch, kw = TINY[name]
-    prob = make_tiny_problem(arch, n_chains=3, seed=hash(name) % 100, noise=0.3, **kw)
+    prob = make_tiny_problem(arch, n_chains=3, seed=TINY_SEED[name], noise=0.3, **kw)
     th = jittered_states(prob, 3)
     with _ctx(prob) as c:
         lp, g = gpu_grad(c, th)
@@ -76,10 +81,18 @@ def test_grad_tiny(name):
         assert_grad_close(lp[ci], g[ci], lr, gr, f"{name} chain {ci}")
 
 
+@pytest.fixture
+def simt_engine():
+    """Contexts set up inside the test run every GEMM on the SIMT engine (hmc_debug_set_engine)."""
+    from paper_2507_14652_b200 import abi
+    abi.hmc_debug_set_engine(1)
+    yield
+    abi.hmc_debug_set_engine(0)
+
+
 @pytest.mark.parametrize("name", ["mlp_ragged", "deeponet_ragged"])
-def test_grad_simt_engine_forced(name, monkeypatch):
-    """The SIMT engine alone (HMC_ENGINE=simt) meets the same tolerances."""
-    monkeypatch.setenv("HMC_ENGINE", "simt")
+def test_grad_simt_engine_forced(name, simt_engine):
+    """The SIMT engine alone meets the same tolerances."""
     arch, kw = TINY[name]
     prob = make_tiny_problem(arch, n_chains=2, seed=11, noise=0.3, **kw)
     th = jittered_states(prob, 2)
@@ -93,17 +106,21 @@ def test_grad_simt_engine_forced(name, monkeypatch):
         assert_grad_close(lp[ci], g[ci], lr, gr, name)
 
 
-def test_grad_cfg5_engines_agree(monkeypatch):
+def test_grad_cfg5_engines_agree():
     """cfg5 gradient: tcgen05 engine vs SIMT engine vs oracle (chain 0)."""
+    from paper_2507_14652_b200 import abi
     prob = make_problem("cfg5", n_chains=4)
     th = jittered_states(prob, 4)
     with _ctx(prob) as c:
-        from paper_2507_14652_b200 import abi
         assert "tcgen05" in abi.hmc_engine_info(c.ctx)
         lp_tc, g_tc = gpu_grad(c, th)
-    monkeypatch.setenv("HMC_ENGINE", "simt")
-    with _ctx(prob) as c:
-        lp_s, g_s = gpu_grad(c, th)
+    abi.hmc_debug_set_engine(1)
+    try:
+        with _ctx(prob) as c:
+            assert abi.hmc_engine_info(c.ctx) == "simt"
+            lp_s, g_s = gpu_grad(c, th)
+    finally:
+        abi.hmc_debug_set_engine(0)
     t = ohmc.Target(prob)
     lr, gr = t.logp_grad(th[0])
     assert_grad_close(lp_tc[0], g_tc[0], lr, gr, "tc")
@@ -399,11 +416,20 @@ def test_config_errors_are_reported():
         with pytest.raises(abi.HmcError) as e:
             abi.Context(p2)
         assert e.value.code == abi.HMC_E_CONFIG
+    # world / shard validation: world in {1, 2, 4, 8}, SINGLE needs world 1,
+    # DATA mode needs equal shards (more in test_gpu_contract.py)
+    for kw in (dict(mode="chain", world=3), dict(mode="single", world=2), dict(mode="data", world=1, n_global=9)):
+        with pytest.raises(abi.HmcError) as e:
+            abi.Context(prob, **kw)
+        assert e.value.code == abi.HMC_E_CONFIG, kw
     with abi.Context(prob) as c:
         th = jittered_states(prob, 1)
         lp, g = gpu_grad(c, th)
-        with pytest.raises(abi.HmcError):
-            abi.hmc_trajectory(c.ctx, th, lp, g, -1.0, 5, 0)
+        for bad in (dict(eps=-1.0, L=5, it=0), dict(eps=float("nan"), L=5, it=0), dict(eps=1e-3, L=-1, it=0),
+                    dict(eps=1e-3, L=5, it=1 << 32), dict(eps=0.0, L=5, it=0)):   # eps 0 before hmc_adapt
+            with pytest.raises(abi.HmcError) as e:
+                abi.hmc_trajectory(c.ctx, th, lp, g, bad["eps"], bad["L"], bad["it"])
+            assert e.value.code == abi.HMC_E_CONFIG, bad
 
 
 @pytest.mark.parametrize("name", ["mlp_ragged", "deeponet_ragged"])

@@ -175,3 +175,10 @@ def test_nonfinite_proposal_rejected():
     r = ohmc.trajectory(t, th, lp, g, 0.01, 3, 0, 0)
     assert not r["accepted"]
     np.testing.assert_array_equal(r["theta"], th)
+
+
+def test_divergence_flag_definition():
+    """SPEC S:445 threshold as a flag (Q5): non-finite or |dH| > 1000."""
+    assert ohmc.divergent(float("nan")) and ohmc.divergent(float("inf")) and ohmc.divergent(-float("inf"))
+    assert ohmc.divergent(1000.5) and ohmc.divergent(-1e4)
+    assert not ohmc.divergent(1000.0) and not ohmc.divergent(-999.0) and not ohmc.divergent(0.0)
