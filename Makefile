@@ -7,10 +7,11 @@ FLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xptxas -v --expt-rel
 # from the environment (include/hmc.h "developer knobs"); the product build ignores them
 ifeq ($(DEV),1)
 FLAGS += -DHMC_DEV
+LIB_OUT := paper_2507_14652_b200/libhmc_dev.so
 endif
 SRC := paper_2507_14652_b200/csrc/hmc.cu
 DEPS := $(wildcard paper_2507_14652_b200/csrc/*.cuh) include/hmc.h
-LIB := paper_2507_14652_b200/libhmc.so
+LIB := $(or $(LIB_OUT),paper_2507_14652_b200/libhmc.so)
 # link the NCCL that ships with torch (same soname, newer than the system copy) and find it at run time
 PYTHON ?= python
 NCCL_LIB := $(shell $(PYTHON) -c "import os, nvidia.nccl as m; print(os.path.join(list(m.__path__)[0], 'lib'))" 2>/dev/null)

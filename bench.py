@@ -7,9 +7,14 @@ full-batch forward + backward over the whole training set, then the Metropolis t
 value = chain gradient evaluations per second summed over all GPUs (C x L x K x N / t_max).
 
 Default workload: cfg5 (cone-surface DeepONet, 528,641 params, 20,000 active, 512 x 2048 pairs,
-64 chains, L = 200) - the north-star target config; `--cfg` selects another.
-N > 1 (torchrun): chain-parallel, C chains per GPU with global chain ids, no data-path collective
-("scaling": "weak").  `--impl reference` times the fp64 CPU oracle (the reference arm).
+64 chains, L = 200) - the north-star target config; `--cfg` selects another (cfg1..cfg5, cfg4u).
+Step size: cfg4 / cfg5 sample at the dual-averaged eps for 80 % acceptance (their configured
+eps diverges - DESIGN.md §3), timed beside one run at the configured eps; the others at their eps.
+N > 1 (torchrun): cfg5 / cfg3 run DATA mode - one chain set over the training set sharded across
+the GPUs (cfg5 POINTS_XB: all-gather of branch outputs, reduce-scatter of dB, all-reduce of the
+k-gradient in-graph with NCCL; "scaling": "strong"); the other configs run chain-parallel (each GPU
+its own chains, no collective; "weak").  `--parallel` overrides.  `--impl reference` times the fp64
+CPU oracle (the reference arm).
 """
 from __future__ import annotations
 
@@ -99,8 +104,10 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------- CPU oracle ---
-def cpu_oracle_rate(prob, budget_s=12.0, min_evals=3):
-    """fp64 oracle full-batch gradient evaluations / s on this host (chain 0, initial state)."""
+def cpu_oracle_rate(prob, budget_s=12.0, min_evals=5):
+    """fp64 oracle full-batch gradient evaluations on this host (chain 0, initial state): the
+    median of >= 5 single-evaluation times (SURVEY §8(d) "Timing (oracle)"), repeated for about
+    budget_s seconds."""
     from oracle import hmc as ohmc
     try:
         from threadpoolctl import threadpool_info
@@ -110,13 +117,17 @@ def cpu_oracle_rate(prob, budget_s=12.0, min_evals=3):
     t = ohmc.Target(prob)
     th = prob.frozen[prob.idx].astype(np.float64)
     t.logp_grad(th)   # warm
-    n, t0 = 0, time.perf_counter()
-    while n < min_evals or time.perf_counter() - t0 < budget_s:
+    times, t0 = [], time.perf_counter()
+    while len(times) < min_evals or time.perf_counter() - t0 < budget_s:
+        a = time.perf_counter()
         t.logp_grad(th)
-        n += 1
-    dt = time.perf_counter() - t0
+        times.append(time.perf_counter() - a)
+    med = statistics.median(times)
     cores = len(os.sched_getaffinity(0))
-    return n / dt, n, dt, cores, threads
+    return {"value": 1.0 / med, "unit": "evals/s", "cores": cores, "kind": "oracle", "blas_threads": threads,
+            "seconds_per_eval_median": med, "evals_timed": len(times),
+            "sample": f"{len(times)} full-batch fp64 gradient evaluations of chain 0 at the initial state "
+                      f"({sum(times):.1f} s; value = 1 / median time per evaluation; NumPy/OpenBLAS oracle as it stands)"}
 
 
 def run_reference(args):
@@ -132,12 +143,13 @@ def run_reference(args):
     th = prob.frozen[prob.idx].astype(np.float64)
     lp, g = t.logp_grad(th)
     Lr = args.ref_L
+    eps = STABLE_EPS0.get(args.cfg, prob.eps)   # a step that does not diverge (as our arm's adapted eps)
     for w in range(args.warmup):
-        r = ohmc.trajectory(t, th, lp, g, prob.eps, Lr, w, 0)
+        r = ohmc.trajectory(t, th, lp, g, eps, Lr, w, 0)
         th, lp, g = r["theta"], r["logp"], r["grad"]
     t0 = time.perf_counter()
     for s in range(args.steps):
-        r = ohmc.trajectory(t, th, lp, g, prob.eps, Lr, args.warmup + s, 0)
+        r = ohmc.trajectory(t, th, lp, g, eps, Lr, args.warmup + s, 0)
         th, lp, g = r["theta"], r["logp"], r["grad"]
     dt = time.perf_counter() - t0
     evals = Lr * args.steps
@@ -157,11 +169,28 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm ---
+# 0.25 x the leapfrog stability limit 2 / sqrt(lambda_max) at the seeded state (DESIGN.md §3
+# "step sizes"): the dual-averaging warm-up of cfg4 / cfg5 starts here, because the
+# configured eps of those configs is 11x / 15x beyond the limit (every proposal diverges).
+STABLE_EPS0 = {"cfg4": 1.1e-6, "cfg4u": 1.1e-6, "cfg5": 4.0e-7}
+# DATA-mode layout per config for N > 1; configs not listed run chain-parallel
+DATA_SHARD = {"cfg3": "rows", "cfg5": "points_xb"}
+
+
+def _parallel(args, world):
+    if world == 1:
+        return "single", None
+    if args.parallel == "chain" or (args.parallel == "auto" and args.cfg not in DATA_SHARD):
+        return "chain", None
+    return "data", DATA_SHARD.get(args.cfg, "rows")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     from hmcdata import make_problem
     from paper_2507_14652_b200 import abi
+    from paper_2507_14652_b200 import dist as pdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -175,13 +204,20 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
 
     prob = make_problem(args.cfg)
-    C, k, L, eps = prob.n_chains, prob.k, prob.L, prob.eps
+    C, k, L = prob.n_chains, prob.k, prob.L
     if args.L:
         L = args.L
-    if args.eps:
-        eps = args.eps
-    ids = (rank * C + np.arange(C)).astype(np.uint32)
-    ctx = abi.Context(prob, mode="chain" if world > 1 else "single", rank=rank, world=world, chain_ids=ids)
+    mode, shard = _parallel(args, world)
+    if mode == "chain":
+        ids = pdist.chain_ids(rank, C)
+        ctx = abi.Context(prob, mode="chain", rank=rank, world=world, chain_ids=ids)
+        scaling, units_per_step = "weak", world * C * L      # every rank: its own C chains
+    elif mode == "data":
+        ctx = pdist.make_context(prob, "data", rank, world, shard=shard)
+        scaling, units_per_step = "strong", C * L            # one chain set over the sharded data
+    else:
+        ctx = abi.Context(prob)
+        scaling, units_per_step = "weak", C * L
 
     th0 = np.repeat(prob.frozen[prob.idx][None, :], C, axis=0).astype(np.float32)  # Q20: start at mu_s
     T = torch.as_tensor(th0, device=dev).contiguous()
@@ -189,18 +225,37 @@ def run_ours(args):
     G = torch.empty(C, k, dtype=torch.float32, device=dev)
     abi.hmc_grad(ctx.ctx, T, LP, G)
     K, W = args.steps, args.warmup
+    it = 0
+    # ---- step size: the configured eps, or dual averaging to 80 % acceptance ----
+    eps_mode = args.eps_mode if args.eps_mode != "auto" else ("adapt" if args.cfg in STABLE_EPS0 else "config")
+    if args.eps:
+        eps_mode = "fixed"
+    eps_info = {"mode": eps_mode}
+    if eps_mode == "adapt":
+        eps0 = STABLE_EPS0.get(args.cfg, prob.eps)
+        eps_bar = abi.hmc_adapt(ctx.ctx, T, LP, G, eps0, L, it, args.adapt, 0.8)
+        it += args.adapt
+        eps = 0.0    # every chain at its own adapted eps_bar
+        eps_info.update({"eps0": eps0, "n_adapt": args.adapt, "target_accept": 0.8,
+                         "eps_bar_median": float(np.median(eps_bar)), "eps_bar_min": float(eps_bar.min()),
+                         "eps_bar_max": float(eps_bar.max())})
+    else:
+        eps = args.eps if args.eps else prob.eps
+        eps_info["eps"] = eps
+    acc1 = torch.empty(C, 1, dtype=torch.uint8, device=dev)
+    dH1 = torch.empty(C, 1, dtype=torch.float64, device=dev)
+    for _ in range(W):
+        abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, 1, None, acc1, dH1)
+        it += 1
+    torch.cuda.synchronize()
     smp = torch.empty(C, max(K, 1), k, dtype=torch.float32, device=dev)
     acc = torch.empty(C, max(K, 1), dtype=torch.uint8, device=dev)
     dH = torch.empty(C, max(K, 1), dtype=torch.float64, device=dev)
-    it = 0
-    for _ in range(W):
-        abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, 1, smp, acc, dH)
-        it += 1
-    torch.cuda.synchronize()
     gpu_index = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         gpu_index = vis.split(",")[local]
+    abi.hmc_divergences(ctx.ctx, reset=True)
     clk = Clocks(gpu_index)
     if world > 1:
         dist.barrier()
@@ -219,14 +274,28 @@ def run_ours(args):
         tt = torch.tensor([t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = tt.item()
-    evals = world * C * L * K
-    value = evals / t
+    value = units_per_step * K / t
     acc_rate = acc[:, :K].float().mean().item()
+    divergent = int(abi.hmc_divergences(ctx.ctx).sum())
+
+    # the same work at the configured eps (proposals diverge at cfg4 / cfg5): time per step is set
+    # by L, not by the acceptance (state restored afterwards)
+    cfg_eps_ms = None
+    if eps_mode == "adapt" and not args.no_config_eps:
+        Tc, LPc, Gc = T.clone(), LP.clone(), G.clone()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        abi.hmc_sample(ctx.ctx, Tc, LPc, Gc, prob.eps, L, it, 1, None, acc1, dH1)   # warm
+        a0.record()
+        abi.hmc_sample(ctx.ctx, Tc, LPc, Gc, prob.eps, L, it + 1, 2, None, None, None)
+        a1.record()
+        torch.cuda.synchronize()
+        cfg_eps_ms = a0.elapsed_time(a1) / 2
+        it += 3
 
     # ---- live per-kernel timing: one more (untimed) trajectory with event nodes in the graph; its
     #      first leapfrog step runs on one stream so each kernel is timed alone ----
     abi.hmc_profile(ctx.ctx, True)
-    abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, 1, smp, acc, dH)
+    abi.hmc_sample(ctx.ctx, T, LP, G, eps, L, it, 1, None, acc1, dH1)
     it += 1
     torch.cuda.synchronize()
     prof = abi.hmc_profile_read(ctx.ctx)
@@ -247,16 +316,19 @@ def run_ours(args):
     peaks, peak_src = load_peaks()
     engine = abi.hmc_engine_info(ctx.ctx)
     roofline = None
+    tc_sust = peaks.get("bf16_tflops_sustained", 1393.9) * 0.5 / 3.0
+    tc_burst = peaks.get("bf16_tflops", 1590.0) * 0.5 / 3.0
+    simt_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     if dom:
         name, (ms, fl, by, nl) = dom
         achieved = fl / (ms / 1000.0) / 1e12
         if name.startswith("tc_"):
-            peak = peaks.get("bf16_tflops_sustained", 1393.9) * 0.5 / 3.0
+            peak, peak_alt = tc_sust, tc_burst
             bound, unit = "tensor", "TFLOP/s"
             peak_note = (f"FP32-equivalent 3xTF32 peak = {peak_src} bf16 sustained x 0.5 (TF32/BF16 "
-                         f"nominal ratio) / 3")
+                         f"nominal ratio) / 3; peak_burst from the burst bf16 figure")
         else:
-            peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+            peak, peak_alt = simt_peak, None
             bound, unit = "alu", "TFLOP/s"
             peak_note = "SIMT FP32 FMA peak = 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md §5)"
         traffic = None
@@ -275,6 +347,21 @@ def run_ours(args):
                     "launches_per_eval": nl, "ms_per_eval": ms,
                     "share_of_step0": ms / step0_total if step0_total else None,
                     "algorithmic_flops_per_eval": fl, "peak_source": peak_note}
+        if peak_alt:
+            roofline["peak_burst"] = peak_alt
+            roofline["frac_burst"] = achieved / peak_alt
+    # whole gradient evaluation (all chains) against the binding peak: F_eval of SURVEY §8(d)
+    f_eval = F_EVAL.get(args.cfg)
+    whole = None
+    if f_eval and body_ms:
+        ev_ms = statistics.median(body_ms)
+        tf_whole = f_eval * C / (ev_ms / 1000.0) / 1e12
+        narrow = engine.startswith("narrow")
+        whole = {"F_eval_per_chain": f_eval, "eval_ms_median": ev_ms, "achieved": tf_whole,
+                 "peak": simt_peak if narrow else tc_sust, "bound": "alu" if narrow else "tensor",
+                 "frac": tf_whole / (simt_peak if narrow else tc_sust)}
+        if not narrow:
+            whole["frac_burst"] = tf_whole / tc_burst
 
     # ---- e2e: same metric through the C-ABI with pinned host buffers (H2D/D2H inside) ----
     e2e = None
@@ -303,41 +390,50 @@ def run_ours(args):
             te = tt.item()
         h2d = C * k * 4 * 2 + C * 8
         d2h = h2d + C * k * 4 + C + C * 8
-        e2e = {"value": world * C * L * Ke / te, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": units_per_step * Ke / te, "unit": "evals/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": Ke, "clocks": clocks_e2e}
 
     per_grad, base, per_step = abi.hmc_launch_counts(ctx.ctx)
     launches = K * (base + L * per_step)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, n, dt, cores, threads = cpu_oracle_rate(prob, budget_s=args.cpu_budget)
-        cpu = {"value": rate, "unit": "evals/s", "cores": cores, "kind": "oracle",
-               "blas_threads": threads,
-               "sample": f"{n} full-batch fp64 gradient evaluations of chain 0 at the initial state "
-                         f"({dt:.1f} s, NumPy/OpenBLAS oracle as it stands)"}
-    mode = "chain-parallel" if world > 1 else "single"
+        cpu = cpu_oracle_rate(prob, budget_s=args.cpu_budget)
+    desc = {"single": "single", "chain": "chain-parallel", "data": f"data-parallel ({shard})"}[mode]
     out = {"metric": "full-batch masked-gradient evals/sec", "value": value, "unit": "evals/s",
            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": 1000 * t / K,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (seeded generators of SURVEY §8(d); random-init frozen means)",
-           "config": {"workload": WORKLOAD_DESC[args.cfg], "chains_per_gpu": C, "L": L, "eps": eps,
-                      "P": prob.P, "k": k, "parallelism": f"{mode} x{world}", "engine": engine,
+           "config": {"workload": WORKLOAD_DESC[args.cfg], "chains": C, "L": L, "eps": eps_info,
+                      "P": prob.P, "k": k, "parallelism": f"{desc} x{world}", "engine": engine,
                       "step": "one HMC iteration (L leapfrog steps + MH) of every chain",
-                      "eps_note": "configured eps; cfg4/cfg5 eps exceed the leapfrog stability limit "
-                                  "at the seeded state (DESIGN.md §3), proposals diverge and are "
-                                  "rejected; work per step is fixed by L",
-                      "l2": "inputs larger than L2: per-step working set (activations of all chains) "
-                            "exceeds the 126 MB L2, no flush needed"},
-           "samples_per_s": world * C * K / t, "acceptance": acc_rate,
+                      "units": ("gradient evaluations of the whole job: chains x L per step"
+                                + (" x GPUs (each GPU its own chains)" if mode == "chain" else "")),
+                      "l2": L2_NOTE.get(args.cfg, L2_NOTE["default"])},
+           "samples_per_s": (world if mode == "chain" else 1) * C * K / t, "acceptance": acc_rate,
+           "divergent_trajectories": divergent, "config_eps_ms_per_step": cfg_eps_ms,
            "eval_ms_mean": (statistics.mean(body_ms) if body_ms else None),
            "body_flops_per_eval_all_chains": body_flops,
-           "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-           "clocks": clocks}
+           "gpu_launches": launches, "roofline": roofline, "whole_eval": whole, "cpu_baseline": cpu,
+           "e2e": e2e, "clocks": clocks}
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# F_eval = 6 N P (MLP) or 6 (N_c P_b + N_x P_t) + 6 N_c N_x p (factored DeepONet)
+F_EVAL = {"cfg1": 1.847e5, "cfg2": 7.787e7, "cfg3": 1.3188e10, "cfg4": 4.31e8, "cfg5": 5.667e9}
+L2_NOTE = {
+    "default": "inputs larger than L2: per-step working set (activations of all chains) exceeds the 126 MB L2, "
+               "no flush needed",
+    "cfg1": "resident by design: the narrow engine keeps weights and activations in shared memory across "
+            "steps (the whole working set is on chip; no L2 flush applies)",
+    "cfg2": "resident by design: the narrow engine keeps weights and activations in shared memory across "
+            "steps (the whole working set is on chip; no L2 flush applies)",
+    "cfg4": "working set (activations of 16 chains, ~35 MB) fits in L2 and stays there between steps, as in "
+            "production; no flush",
+}
 
 
 def main():
@@ -354,10 +450,20 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="per-kernel-class times of step 0 to stderr")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "data", "chain"],
+                    help="N > 1: data = shard the training set (cfg5 POINTS_XB, else rows; strong scaling), "
+                         "chain = independent chains per GPU (weak scaling); auto = data for cfg3 / cfg5")
+    ap.add_argument("--eps-mode", default="auto", choices=["auto", "config", "adapt"],
+                    help="auto: dual averaging to 80%% acceptance (P:490) for cfg4 / cfg5, configured eps otherwise")
+    ap.add_argument("--adapt", type=int, default=12, help="dual-averaging warm-up trajectories (eps-mode adapt)")
+    ap.add_argument("--no-config-eps", action="store_true", help="skip the configured-eps timing beside an adapted run")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: the contract needs >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # init lines for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference(args)
     else:

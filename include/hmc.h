@@ -234,9 +234,10 @@ const char* hmc_engine_info(const hmc_ctx* ctx);
  * the context's stream.  HMC_E_CONFIG on NULL counts. */
 int hmc_divergences(hmc_ctx* ctx, uint32_t* counts, int32_t reset);
 
-/* Test hook: mode 1 makes contexts set up afterwards (process-wide) run every GEMM on the SIMT
- * FP32 engine, 0 restores the automatic choice (tcgen05 wherever it takes the shape).  Returns
- * HMC_E_CONFIG for any other mode.  Developer knobs of the tcgen05 engine (HMC_TC_* environment
+/* Test hook, process-wide, read by hmc_setup: mode 0 = automatic (the narrow-network cluster
+ * engine for MLPs that qualify, else tcgen05 wherever it takes the shape and SIMT elsewhere);
+ * 1 = every GEMM on the per-layer SIMT FP32 engine; 2 = the per-layer engines only (no narrow
+ * engine).  Returns HMC_E_CONFIG for any other mode.  Developer knobs of the tcgen05 engine (HMC_TC_* environment
  * variables: barrier profiles, timelines, A/B toggles) are compiled in only with -DHMC_DEV
  * (`make DEV=1`); the product library ignores the environment. */
 int hmc_debug_set_engine(int32_t mode);

@@ -22,6 +22,7 @@
 #include "../../include/hmc.h"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "narrow.cuh"
 #include "partition.cuh"
 #include "tc_gemm.cuh"
 
@@ -168,6 +169,11 @@ struct hmc_ctx {
   std::string err;
   std::string engine;
   TcPlanner tc;
+  // narrow-network engine (csrc/narrow.cuh): whole leapfrog steps in one cluster kernel per chain
+  bool narrow = false;
+  nw::NarrowArgs nwa;
+  int nw_hw = 0, nw_clusters = 0;  // template instantiation (uniform hidden width), co-resident clusters
+  int32_t* d_soff = nullptr;
 
   KState kstate() const {
     KState s;
@@ -829,6 +835,173 @@ void enqueue_sensitivity(hmc_ctx* x, std::string& err) {
   CK(cudaGetLastError());
 }
 
+// Narrow-network engine planning (csrc/narrow.cuh): an MLP whose hidden layers are tanh /
+// identity with widths that are multiples of 4 (<= 128) runs whole leapfrog steps in one kernel,
+// a cluster of nc CTAs per chain with the weights and the rows' activations resident in shared
+// memory.  nc and the rows per CTA depend on the per-chain problem and the device only (batch
+// invariance).  Returns false (the per-layer engines run) when the network does not qualify.
+int nw_pad(int w) {
+  int p = (w + 3) / 4 * 4;
+  return (p % 8 == 0) ? p + 4 : p;  // row stride = 4 (mod 8) floats: float4 rows spread over the banks
+}
+
+bool nw_layout(hmc_ctx* x, int bpc, int nc, nw::NarrowArgs& a) {
+  const NetInfo& N = x->nets[0];
+  const int rows = bpc * a.rb;
+  int off = 0;
+  for (int l = 0; l < a.nl; ++l) {
+    const LayerInfo& L = x->layers[N.layers[l]];
+    a.ldw[l] = nw_pad(L.n_in);
+    a.sw[l] = off;
+    off += L.n_out * a.ldw[l];
+    a.sb[l] = off;
+    off += (L.n_out + 3) / 4 * 4;
+  }
+  for (int l = 0; l < a.nl; ++l) {
+    a.lda[l] = nw_pad(a.width[l]);
+    a.sa[l] = off;
+    off += rows * a.lda[l];
+  }
+  a.s_r = off;
+  off += (rows + 3) / 4 * 4;
+  a.s_rr = off;
+  off += (rows + 3) / 4 * 4;
+  a.ksp = (int)(((x->k + nc - 1) / nc + 3) / 4 * 4);  // k-slice per CTA (multiple of 4)
+  a.kp = nc * a.ksp;
+  a.s_gp = off;    // this CTA's block partials [bpc x kp]
+  off += bpc * a.kp;
+  a.s_recv = off;  // receive buffer: the nblk block partials of this CTA's k-slice
+  off += a.nblk * a.ksp;
+  a.s_sl = off;
+  off += 2 * a.ksp;
+  a.s_y = off;
+  off += (rows + 3) / 4 * 4;
+  a.s_slot = off;
+  a.slot16 = x->k < 32768 ? 1 : 0;
+  off += (int)((x->P * (a.slot16 ? 2 : 4) + 15) / 16 * 4);
+  off = (off + 3) / 4 * 4;
+  a.s_red = off;
+  off += 2 * (nw::NBMAX + 1 + 8);  // doubles: per-block sum r^2, sum theta^2, block_sum_d scratch
+  a.bpc = bpc;
+  a.smem_bytes = off * 4;
+  return true;
+}
+
+// Row blocks (the unit of every sum over data rows, so a function of the problem only):
+// rb = max(16, ceil(n / NBMAX)) rounded to 4, nblk = ceil(n / rb).  Cluster size nc and blocks per
+// CTA bpc (results do not depend on them): the feasible (shared memory, co-resident cluster)
+// choice with the fewest block-times per chain batch, ceil(C / active clusters) x bpc.
+bool plan_narrow(hmc_ctx* x, std::string& err) {
+  if (x->kind != HMC_MLP || x->mode == HMC_MODE_DATA || engine_override() != 0) return false;
+  const NetInfo& N = x->nets[0];
+  const int nl = (int)N.layers.size();
+  if (nl > nw::MAXL || N.l_min < 0) return false;
+  nw::NarrowArgs a;
+  memset(&a, 0, sizeof(a));
+  a.nl = nl;
+  int hw = -1;  // uniform hidden width (template instantiation), 0 = mixed
+  for (int l = 0; l < nl; ++l) {
+    const LayerInfo& L = x->layers[N.layers[l]];
+    if (l < nl - 1 && (L.act == ACT_SIN || L.n_out % 4 != 0 || L.n_out > 128)) return false;
+    if (l == 0 && L.n_in > 64) return false;
+    if (l < nl - 1) hw = (hw == -1 || hw == L.n_out) ? L.n_out : 0;
+    a.width[l] = L.n_in;
+    a.width[l + 1] = L.n_out;
+    a.act[l] = L.act;
+    a.w_off[l] = L.w_off;
+    a.b_off[l] = L.bias ? L.b_off : -1;
+  }
+  if (hw != 16 && hw != 32 && hw != 64 && hw != 128) hw = 0;
+  a.l_min = N.l_min;
+  a.n = x->n;
+  if (const char* e = dev_env("HMC_NW_DBG")) a.dbg = atoi(e);
+  a.rb = (int)std::max<int64_t>(16, ((x->n + nw::NBMAX - 1) / nw::NBMAX + 3) / 4 * 4);
+  a.nblk = (int)((x->n + a.rb - 1) / a.rb);
+  int dev = 0, optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const void* fn = nw::narrow_kernel(hw);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  double best = 1e30;
+  for (int nc = std::min(nw::NCMAX, a.nblk); nc >= 1; --nc) {
+    const int bpc = (a.nblk + nc - 1) / nc;
+    if ((nc - 1) * bpc >= a.nblk) continue;  // no CTA without a row block
+    nw::NarrowArgs t = a;
+    nw_layout(x, bpc, nc, t);
+    if (t.smem_bytes > optin) continue;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(nc);
+    cfg.blockDim = dim3(nw::NT);
+    cfg.dynamicSmemBytes = t.smem_bytes;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = nc;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (clusters < 1) continue;
+    const double cost = (double)((x->C + clusters - 1) / clusters) * bpc;
+    if (cost < best - 1e-9) {
+      best = cost;
+      t.nc = nc;
+      x->nwa = t;
+      x->nw_hw = hw;
+      x->nw_clusters = clusters;
+    }
+  }
+  if (best >= 1e30) return false;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x->nwa.smem_bytes));
+  return true;
+}
+
+void launch_narrow(hmc_ctx* x, int nsteps, int last_mode, cudaStream_t st, std::string& err) {
+  nw::NarrowArgs a = x->nwa;
+  a.x = x->d_x;
+  a.y = x->d_y;
+  a.slot = x->d_slot;
+  a.soff = x->d_soff;
+  a.inv_s2 = (float)(1.0 / (x->sigma * x->sigma));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(x->C * a.nc));
+  cfg.blockDim = dim3(nw::NT);
+  cfg.dynamicSmemBytes = a.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = a.nc;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  KState ks = x->kstate();
+  void* args[] = {&ks, &a, &nsteps, &last_mode};
+  CK(cudaLaunchKernelExC(&cfg, nw::narrow_kernel(x->nw_hw), args));
+  x->launches++;
+}
+
+// flops of one narrow-engine gradient evaluation of all chains (forward + input-gradient + dense
+// weight-gradient tiles, 2 per multiply-add; the bench's roofline numerator)
+double narrow_flops(const hmc_ctx* x) {
+  const nw::NarrowArgs& a = x->nwa;
+  double f = 0.0;
+  for (int l = 0; l < a.nl; ++l) {
+    const double mac = (double)a.width[l] * a.width[l + 1] * (double)x->n;
+    f += 2.0 * mac;                                  // forward
+    if (l >= a.l_min) f += 2.0 * mac;                // weight gradient
+    if (l > a.l_min) f += 2.0 * mac;                 // input gradient
+  }
+  return f * x->C;
+}
+
 void capture_begin(hmc_ctx* x, std::string& err) {
   CK(cudaStreamBeginCapture(x->st, cudaStreamCaptureModeThreadLocal));
 }
@@ -854,11 +1027,16 @@ void build_grad_graph(hmc_ctx* x, std::string& err) {
   try {
     k_scatter<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, x->st>>>(x->kstate(), x->wrk_theta);
     x->launches++;
-    enqueue_body(x, x->st);
-    x->per_body = x->launches - l0 - 1;
-    enqueue_reduce(x, x->st, err);
-    k_finalize<<<x->C, KT, 0, x->st>>>(x->kstate(), 0);
-    x->launches++;
+    if (x->narrow) {  // forward + gradient + prior + log pi in one cluster kernel
+      launch_narrow(x, 1, 0, x->st, err);
+      x->per_body = 1;
+    } else {
+      enqueue_body(x, x->st);
+      x->per_body = x->launches - l0 - 1;
+      enqueue_reduce(x, x->st, err);
+      k_finalize<<<x->C, KT, 0, x->st>>>(x->kstate(), 0);
+      x->launches++;
+    }
   } catch (...) {
     cudaGraph_t g;
     cudaStreamEndCapture(x->st, &g);
@@ -882,10 +1060,27 @@ void build_traj_graph(hmc_ctx* x, int L, std::string& err) {
     int id = prof_begin(x, x->st);
     k_traj_begin<<<x->C, KT, 0, x->st>>>(x->kstate(), L == 0 ? 1 : 0);
     prof_end(x, id, x->st, "traj_begin", 0.0, 0.0);
-    for (int s = 0; s < L; ++s) {
-      x->prof_step = s;
-      x->prof_armed = x->prof_on && s == 0;
-      enqueue_step(x, s == L - 1 ? 2 : 1, x->st, err);
+    if (x->narrow && L > 0) {
+      if (x->prof_on) {  // profiled trajectory: one launch per step, each timed
+        const double fl = narrow_flops(x);
+        for (int s = 0; s < L; ++s) {
+          x->prof_step = s;
+          x->prof_armed = s == 0;
+          const int idb = prof_begin(x, x->st, true);
+          const int idk = prof_begin(x, x->st);  // step 0: the kernel record (same launch)
+          launch_narrow(x, 1, s == L - 1 ? 2 : 1, x->st, err);
+          prof_end(x, idk, x->st, "narrow_step", fl, 0.0);
+          prof_end(x, idb, x->st, "body", fl, 0.0);
+        }
+      } else {
+        launch_narrow(x, L, 2, x->st, err);  // all L leapfrog steps in one launch
+      }
+    } else {
+      for (int s = 0; s < L; ++s) {
+        x->prof_step = s;
+        x->prof_armed = x->prof_on && s == 0;
+        enqueue_step(x, s == L - 1 ? 2 : 1, x->st, err);
+      }
     }
     x->prof_step = -1;
     x->prof_armed = x->prof_on;
@@ -943,7 +1138,8 @@ void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, in
 }
 
 // ---------------------------------------------------------------------------------------------
-void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, std::string& err) {
+void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, std::string& err,
+                bool allow_narrow = true) {
   CFG(arch && data && cfg, "arch, data and config must be non-NULL");
   CFG(arch->kind == HMC_MLP || arch->kind == HMC_DEEPONET, "arch.kind must be HMC_MLP or HMC_DEEPONET");
   x->kind = arch->kind;
@@ -1081,7 +1277,13 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   // ---- tensor-core engine: which layers keep tf32 hi/lo weight planes ----
   x->tc.init();
   std::vector<int32_t> tcpos((size_t)x->k, -1);
-  if (x->tc.enabled) {
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    NetInfo& N = x->nets[ni];
+    for (int i = 0; i < (int)N.layers.size(); ++i)
+      if (x->layers[N.layers[i]].any_active) { N.l_min = i; break; }
+  }
+  x->narrow = allow_narrow && plan_narrow(x, err);
+  if (x->tc.enabled && !x->narrow) {
     for (int ni = 0; ni < x->n_nets; ++ni) {
       NetInfo& N = x->nets[ni];
       for (int i = 0; i < (int)N.layers.size(); ++i) {
@@ -1176,6 +1378,23 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   CK(cudaMemcpy(x->d_slot, slot.data(), x->P * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(x->d_chain, h_ch.data(), C * 4, cudaMemcpyHostToDevice));
   if (!h_im.empty()) CK(cudaMemcpy(x->d_inv_mass, h_im.data(), x->k * 4, cudaMemcpyHostToDevice));
+  if (x->narrow) {  // shared-memory word of every active entry in the narrow engine's weight copy
+    std::vector<int32_t> soff((size_t)x->k, -1);
+    const NetInfo& N = x->nets[0];
+    for (int64_t j = 0; j < x->k; ++j)
+      for (int l = 0; l < x->nwa.nl; ++l) {
+        const LayerInfo& L = x->layers[N.layers[l]];
+        const int64_t f = h_idx[j];
+        if (f >= L.w_off && f < L.w_off + (int64_t)L.n_in * L.n_out) {
+          const int64_t o = (f - L.w_off) / L.n_in, i = (f - L.w_off) % L.n_in;
+          soff[j] = x->nwa.sw[l] + (int32_t)(o * x->nwa.ldw[l] + i);
+        } else if (L.bias && f >= L.b_off && f < L.b_off + L.n_out) {
+          soff[j] = x->nwa.sb[l] + (int32_t)(f - L.b_off);
+        }
+      }
+    x->d_soff = dalloc<int32_t>(x, x->k, err);
+    CK(cudaMemcpy(x->d_soff, soff.data(), x->k * 4, cudaMemcpyHostToDevice));
+  }
   for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
   if (x->Ptc > 0) {
     x->Whi = dalloc<float>(x, (size_t)C * x->Ptc, err);
@@ -1325,7 +1544,10 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     }
     CKN(ncclCommInitRank(&x->comm, x->world, id, x->rank));
   }
-  x->engine = x->tc.describe();
+  x->engine = x->narrow ? "narrow-simt (cluster " + std::to_string(x->nwa.nc) + " x " + std::to_string(x->nwa.bpc) +
+                              " blocks of " + std::to_string(x->nwa.rb) + " rows, " + std::to_string(x->nwa.nblk) +
+                              " blocks, hw " + std::to_string(x->nw_hw) + ")"
+                        : x->tc.describe();
   CK(cudaDeviceSynchronize());
 }
 
@@ -1703,7 +1925,7 @@ int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu,
     cfg.n_chains = arch->kind == HMC_DEEPONET ? p : 1;
     cfg.mode = HMC_MODE_SINGLE;
     cfg.world = 1;
-    setup_impl(x.get(), arch, data, &cfg, err);
+    setup_impl(x.get(), arch, data, &cfg, err, false);  // (the per-layer engines' squared-operand mode)
     enqueue_sensitivity(x.get(), err);
     float* dsig = dalloc<float>(x.get(), (size_t)P, err);
     double* dout = dalloc<double>(x.get(), (size_t)P, err);
@@ -1743,6 +1965,12 @@ int hmc_launch_counts(const hmc_ctx* ctx, int64_t* per_grad, int64_t* per_traj_b
     } catch (Fail f) {
       return f.code;
     }
+  }
+  if (x->narrow) {  // scatter + the cluster kernel; begin + one kernel for all steps + MH + advance
+    if (per_grad) *per_grad = 2;
+    if (per_traj_base) *per_traj_base = 4;
+    if (per_step) *per_step = 0;
+    return HMC_OK;
   }
   if (per_grad) *per_grad = x->per_body + 3;
   if (per_traj_base) *per_traj_base = 3;
@@ -1784,9 +2012,28 @@ int hmc_momentum(hmc_ctx* ctx, int64_t iter, float* p, void* stream) {
 
 const char* hmc_engine_info(const hmc_ctx* ctx) { return ctx ? ctx->engine.c_str() : ""; }
 
+// dev build (-DHMC_DEV): narrow-engine phase cycles of CTA 0 (fwd, output, backward, barrier 1,
+// reduction + update, barrier 2, tail), summed since the last reset
+int hmc_debug_nw_profile(uint64_t* out, int32_t reset) {
+#ifdef HMC_DEV
+  unsigned long long h[10];
+  if (cudaMemcpyFromSymbol(h, nw::g_nwprof, sizeof(h)) != cudaSuccess) return HMC_E_CUDA;
+  if (out) for (int i = 0; i < 10; ++i) out[i] = h[i];
+  if (reset) {
+    memset(h, 0, sizeof(h));
+    if (cudaMemcpyToSymbol(nw::g_nwprof, h, sizeof(h)) != cudaSuccess) return HMC_E_CUDA;
+  }
+  return HMC_OK;
+#else
+  (void)out; (void)reset;
+  g_err = "hmc_debug_nw_profile needs a -DHMC_DEV build (make DEV=1)";
+  return HMC_E_STATE;
+#endif
+}
+
 int hmc_debug_set_engine(int32_t mode) {
-  if (mode != 0 && mode != 1) {
-    g_err = "config: engine mode must be 0 (automatic) or 1 (SIMT only)";
+  if (mode < 0 || mode > 2) {
+    g_err = "config: engine mode must be 0 (automatic), 1 (per-layer SIMT only) or 2 (per-layer engines)";
     return HMC_E_CONFIG;
   }
   engine_override() = mode;
