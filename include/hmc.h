@@ -111,6 +111,9 @@ typedef struct {
                            n_x points (hmc_data.n_c = all conditions, n_c % world == 0); the branch
                            outputs are all-gathered, dB reduce-scattered */
   const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode, world > 1) */
+  int32_t exchange;     /* DATA mode: 0 = in-graph NCCL collectives (the product path); 1 = test hook,
+                           no communicator: the context only runs hmc_debug_data_phase and the caller
+                           performs the cross-rank steps (several ranks emulated on one GPU) */
 } hmc_config;
 
 typedef struct hmc_ctx hmc_ctx;
@@ -234,6 +237,29 @@ const char* hmc_engine_info(const hmc_ctx* ctx);
  * the context's stream.  HMC_E_CONFIG on NULL counts. */
 int hmc_divergences(hmc_ctx* ctx, uint32_t* counts, int32_t reset);
 
+/* Test hook: a DATA-mode gradient evaluation cut at its cross-rank steps, for contexts set up
+ * with hmc_config.exchange = 1 (several ranks' contexts on ONE GPU, run one after another; the
+ * caller does each collective on the host or with its own copies).  Device pointers; synchronous.
+ *  phase 0: in = theta [C x k] f32.  ROWS: runs the rank's whole local evaluation, out = its
+ *           likelihood gradient g_lik [C x k] f32, out2 = its sum of squared residuals [C] f64 (the
+ *           all-reduce's inputs).  POINTS_XB: runs the forward of both nets, out = this rank's
+ *           branch outputs [C x n_c/world x p] f32 (the all-gather's input).
+ *  phase 1: POINTS_XB only: in = the all-gather result [world x C x n_c/world x p]; runs the
+ *           combine / residual and the partial dB; out = the reduce-scatter input [world x C x
+ *           n_c/world x p] (block r for rank r).
+ *  phase 2: POINTS_XB only: in = this rank's reduce-scattered dB block [C x n_c/world x p]; runs
+ *           dT and both nets' backward; out / out2 = g_lik / sum r^2 as in phase 0 (ROWS).
+ *  phase 3: in / in2 = the all-reduced g_lik [C x k] / sum r^2 [C]; adds the prior once; out =
+ *           grad [C x k] f32, out2 = log pi [C] f64 - what hmc_grad returns in DATA mode.
+ * HMC_E_CONFIG on a context without exchange = 1, a bad phase or NULL buffers. */
+int hmc_debug_data_phase(hmc_ctx* ctx, int32_t phase, const void* in, const void* in2, void* out, void* out2,
+                         void* stream);
+/* Test hook: the POINTS_XB permutations alone (device pointers, synchronous): dir 0 maps the
+ * all-gather layout [rank][chain][i][k] to per-chain rows [chain][rank n_loc + i][k], dir 1 the
+ * inverse (the reduce-scatter input).  HMC_E_CONFIG on bad arguments. */
+int hmc_debug_xb_permute(int32_t dir, int32_t C, int32_t G, int64_t n_loc, int32_t p, const float* in, float* out,
+                         void* stream);
+
 /* Test hook, process-wide, read by hmc_setup: mode 0 = automatic (the narrow-network cluster
  * engine for MLPs that qualify, else tcgen05 wherever it takes the shape and SIMT elsewhere);
  * 1 = every GEMM on the per-layer SIMT FP32 engine; 2 = the per-layer engines only (no narrow
@@ -283,6 +309,11 @@ int hmc_debug_tc_profile(uint64_t* out, int32_t reset);
  * rows 16-22: epilogue warp 0 (partial ready, folded, released, emitted; at the tile end: flushed,
  * biased / prefetch landed, parked). */
 int hmc_debug_tc_timeline(uint64_t* out);
+/* Developer build only (-DHMC_DEV, `make DEV=1`; HMC_E_STATE otherwise): clock cycles of CTA 0 of
+ * the narrow-network engine per phase, out[10] (host): forward, output layer, push of the block
+ * partials (+ the last input-gradient GEMM), cluster barrier 1, reduction + update, barrier 2,
+ * tail, input gradients + loop overhead, weight gradients; reset != 0 zeroes them. */
+int hmc_debug_nw_profile(uint64_t* out, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -50,14 +50,16 @@ class hmc_config(ctypes.Structure):
                 ("prior_sigma", ctypes.c_double), ("inv_mass", ctypes.c_void_p),
                 ("seed", ctypes.c_uint64), ("n_chains", ctypes.c_int32),
                 ("chain_ids", ctypes.c_void_p), ("mode", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32), ("shard", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("world", ctypes.c_int32), ("shard", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("exchange", ctypes.c_int32)]
 
 
 EXPORTS = ["hmc_comm_unique_id", "hmc_setup", "hmc_grad", "hmc_logpost_const", "hmc_trajectory",
            "hmc_sample", "hmc_destroy", "hmc_last_error", "hmc_launch_counts", "hmc_philox_words",
            "hmc_momentum", "hmc_engine_info", "hmc_profile", "hmc_profile_read", "hmc_debug_gemm",
            "hmc_debug_tc_profile", "hmc_debug_tc_timeline", "hmc_sensitivity", "hmc_adapt", "hmc_predict",
-           "hmc_diagnostics", "hmc_partition", "hmc_divergences", "hmc_debug_set_engine"]
+           "hmc_diagnostics", "hmc_partition", "hmc_divergences", "hmc_debug_set_engine",
+           "hmc_debug_data_phase", "hmc_debug_xb_permute", "hmc_debug_nw_profile"]
 
 
 class hmc_prof_rec(ctypes.Structure):
@@ -280,6 +282,25 @@ def hmc_divergences(ctx, reset: bool = False):
     return out
 
 
+def hmc_debug_data_phase(ctx, phase, inp=None, inp2=None, out=None, out2=None):
+    """Test hook (include/hmc.h): one phase of a DATA-mode evaluation on an exchange='emulated'
+    context; device tensors."""
+    keep = []
+    L = lib()
+    L.hmc_debug_data_phase.argtypes = [ctypes.c_void_p, ctypes.c_int32] + [ctypes.c_void_p] * 5
+    _check(L.hmc_debug_data_phase(ctx, int(phase), _ptr(inp, keep), _ptr(inp2, keep), _ptr(out, keep),
+                                  _ptr(out2, keep), None), ctx)
+
+
+def hmc_debug_xb_permute(direction, C, G, n_loc, p, inp, out):
+    """Test hook: k_xb_gather (direction 0) or k_xb_scatter (1) on device tensors."""
+    keep = []
+    L = lib()
+    L.hmc_debug_xb_permute.argtypes = [ctypes.c_int32] * 3 + [ctypes.c_int64, ctypes.c_int32] + [ctypes.c_void_p] * 3
+    _check(L.hmc_debug_xb_permute(int(direction), int(C), int(G), int(n_loc), int(p), _ptr(inp, keep),
+                                  _ptr(out, keep), None))
+
+
 def hmc_debug_set_engine(mode: int):
     """Test hook: 1 = contexts set up afterwards run every GEMM on the SIMT engine; 0 = automatic."""
     L = lib()
@@ -435,7 +456,7 @@ class Context:
 
     def __init__(self, problem, mode: str = "single", rank: int = 0, world: int = 1,
                  nccl_id: Optional[bytes] = None, n_global: int = 0, chain_ids=None,
-                 n_chains: Optional[int] = None, shard: str = "rows"):
+                 n_chains: Optional[int] = None, shard: str = "rows", exchange: str = "nccl"):
         keep = []
         arch = problem.arch
         nets = [(n.widths, n.acts, n.bias) for n in arch.nets]
@@ -473,6 +494,7 @@ class Context:
         c.mode = MODE[mode]
         c.rank, c.world = int(rank), int(world)
         c.shard = SHARD[shard]
+        c.exchange = {"nccl": 0, "emulated": 1}[exchange]
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
             keep.append(idbuf)

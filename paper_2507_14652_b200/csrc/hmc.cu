@@ -145,6 +145,8 @@ struct hmc_ctx {
   int traj_L = -1;
   // comm
   ncclComm_t comm = nullptr;
+  bool emulated = false;  // DATA mode without a communicator: the caller performs the exchange
+                          // (hmc_debug_data_phase; test hook)
   // live profiling (event nodes inside the trajectory graph)
   struct ProfRec {
     cudaEvent_t a = nullptr, b = nullptr;
@@ -527,6 +529,62 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
   if (ov) cudaStreamWaitEvent(ms, N.evW[N.l_min], 0);  // all weight gradients done (stream order)
 }
 
+// POINTS_XB after the all-gather of the branch outputs (xb_recv, [rank][chain][i][k]): order them
+// per chain, combine with this rank's points (residual and likelihood partials), the partial dB
+// over these points for all conditions, ordered for the reduce-scatter (xb_send)
+void xb_mid(hmc_ctx* x, cudaStream_t st) {
+  const int C = x->C;
+  NetInfo& Nb = x->nets[0];
+  const LayerInfo& Bl = x->layers[Nb.layers.back()];
+  const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
+  const int p = Bl.n_out;
+  k_xb_gather<<<148 * 4, 256, 0, st>>>(x->xb_recv, x->xb_full, C, x->world, x->n_c_loc, p);
+  x->launches++;
+  {
+    GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
+    a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
+    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+    a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+    a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
+    if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
+    a.inv_s2 = 1.0 / (x->sigma * x->sigma);
+    a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
+    launch_gemm(x, a, true, true, st, "combine");
+  }
+  if (Nb.l_min >= 0) {  // partial dB over this rank's points, all conditions, then the send order
+    GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
+    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+    a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
+    a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
+    launch_gemm(x, a, true, false, st, "dB");
+    k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, C, x->world, x->n_c_loc, p);
+    x->launches++;
+  }
+}
+
+// POINTS_XB after the reduce-scatter of dB into the branch's gradient buffer: dT = R^T B_all
+// (complete locally), then both nets' backward
+void xb_back(hmc_ctx* x, cudaStream_t st) {
+  const int C = x->C;
+  NetInfo& Nb = x->nets[0];
+  NetInfo& Nt = x->nets[1];
+  const LayerInfo& Tl = x->layers[Nt.layers.back()];
+  const int p = Tl.n_out;
+  if (Nb.l_min >= 0) Nb.cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
+  if (Nt.l_min >= 0) {
+    GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
+    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+    a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
+    a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
+    a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
+    if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
+    Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+  }
+  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+  if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+}
+
 // forward + backward of one full-batch gradient evaluation (likelihood part only)
 void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   const int C = x->C;
@@ -601,42 +659,9 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     std::string& err = x->err;  // (CKN reports through it)
     const int64_t blk = (int64_t)C * x->n_c_loc * p;
     CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, st));
-    k_xb_gather<<<148 * 4, 256, 0, st>>>(x->xb_recv, x->xb_full, C, x->world, x->n_c_loc, p);
-    x->launches++;
-    {
-      GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
-      a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
-      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-      a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
-      a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
-      if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
-      a.inv_s2 = 1.0 / (x->sigma * x->sigma);
-      a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
-      launch_gemm(x, a, true, true, st, "combine");
-    }
-    if (Nb.l_min >= 0) {  // partial dB over this rank's points, all conditions; then reduce-scatter
-      GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
-      a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
-      a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-      a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
-      a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
-      launch_gemm(x, a, true, false, st, "dB");
-      k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, C, x->world, x->n_c_loc, p);
-      x->launches++;
-      CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, st));
-      Nb.cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
-    }
-    if (Nt.l_min >= 0) {  // dT = R^T B_all, times act' of the trunk output layer: complete locally
-      GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
-      a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
-      a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
-      a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
-      a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
-      if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
-      Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
-    }
-    if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
-    if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    xb_mid(x, st);
+    if (Nb.l_min >= 0) CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, st));
+    xb_back(x, st);
     return;
   }
   if (x->unaligned) {  // per-pair trunk rows: row-wise combine, then the two output gradients
@@ -1534,7 +1559,9 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     }
   }
   // ---- NCCL (DATA mode) ----
-  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb)) {
+  x->emulated = x->mode == HMC_MODE_DATA && cfg->exchange == 1;
+  CFG(cfg->exchange == 0 || cfg->exchange == 1, "exchange must be 0 (NCCL) or 1 (emulated, test hook)");
+  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb) && !x->emulated) {
     ncclUniqueId id;
     if (x->world > 1) {
       CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");
@@ -1608,6 +1635,10 @@ int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg,
 
 int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream) {
   API_BEGIN(ctx)
+  if (ctx->emulated) {
+    err = "state: an emulated-exchange context (hmc_config.exchange = 1) runs only hmc_debug_data_phase";
+    throw Fail{HMC_E_STATE};
+  }
   CFG(theta && logp && grad, "theta, logp and grad must be non-NULL");
   cudaStream_t us = (cudaStream_t)stream;
   const bool host = !is_device_ptr(theta) || !is_device_ptr(logp) || !is_device_ptr(grad);
@@ -1634,6 +1665,10 @@ static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, doubl
                     int32_t S, float* samples, uint8_t* acc, double* dH, void* stream, int adapt = 0,
                     double delta = 0.0, double* eps_bar = nullptr) {
   API_BEGIN(ctx)
+  if (ctx->emulated) {
+    err = "state: an emulated-exchange context (hmc_config.exchange = 1) runs only hmc_debug_data_phase";
+    throw Fail{HMC_E_STATE};
+  }
   CFG(theta && logp && grad, "theta, logp and grad must be non-NULL");
   CFG(std::isfinite(eps) && (eps > 0 || (eps == 0 && ctx->adapted && !adapt)),
       "eps must be finite and > 0 (or 0 after hmc_adapt: the adapted per-chain steps)");
@@ -2029,6 +2064,79 @@ int hmc_debug_nw_profile(uint64_t* out, int32_t reset) {
   g_err = "hmc_debug_nw_profile needs a -DHMC_DEV build (make DEV=1)";
   return HMC_E_STATE;
 #endif
+}
+
+// Test hook: one DATA-mode gradient evaluation split at its cross-rank steps, for contexts set
+// up with hmc_config.exchange = 1 (no communicator).  The caller runs phase p on every rank's
+// context and performs the collective between phases itself (include/hmc.h).
+int hmc_debug_data_phase(hmc_ctx* ctx, int32_t phase, const void* in, const void* in2, void* out, void* out2,
+                         void* stream) {
+  API_BEGIN(ctx)
+  (void)stream;
+  CFG(ctx->emulated, "hmc_debug_data_phase needs a DATA-mode context set up with exchange = 1");
+  CFG(phase >= 0 && phase <= 3, "phase must be 0..3");
+  hmc_ctx* x = ctx;
+  cudaStream_t st = x->st;
+  const size_t Ck = (size_t)x->C * x->k;
+  const int p = x->kind == HMC_DEEPONET ? x->layers[x->nets[0].layers.back()].n_out : 0;
+  const size_t blk = (size_t)x->C * x->n_c_loc * p;
+  NetInfo& Nb = x->nets[0];
+  auto reduce_out = [&]() {
+    k_reduce_partials<<<x->C, KT, 0, st>>>(x->part_sq, x->part_r, x->n_part, x->lik, x->gl, x->k, x->b0_slot);
+    cpy(out, x->gl, Ck * 4, st, err);
+    cpy(out2, x->lik, (size_t)x->C * 8, st, err);
+  };
+  if (phase == 0) {
+    CFG(in && out && (x->xb || out2), "phase 0: theta in; out (and out2 for the row layout)");
+    cpy(x->wrk_theta, in, Ck * 4, st, err);
+    k_scatter<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, st>>>(x->kstate(), x->wrk_theta);
+    if (x->xb) {  // forward of both nets; out = this rank's branch outputs (the all-gather's input)
+      for (int ni = 0; ni < 2; ++ni)
+        for (int i = 0; i < (int)x->nets[ni].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[ni], i, st);
+      cpy(out, x->layers[Nb.layers.back()].A, blk * 4, st, err);
+    } else {      // row layout: the whole local evaluation; out = g_lik [C x k], out2 = sum r^2 [C]
+      enqueue_body(x, st);
+      reduce_out();
+    }
+  } else if (phase == 1) {
+    CFG(x->xb && in && out, "phase 1 (POINTS_XB): in = all-gathered branch outputs, out = reduce-scatter input");
+    cpy(x->xb_recv, in, blk * x->world * 4, st, err);
+    xb_mid(x, st);
+    if (Nb.l_min >= 0) cpy(out, x->xb_send, blk * x->world * 4, st, err);
+    else CK(cudaMemsetAsync(out, 0, blk * x->world * 4, st));
+  } else if (phase == 2) {
+    CFG(x->xb && in && out && out2, "phase 2 (POINTS_XB): in = reduce-scattered dB block, out / out2 = g_lik / sum r^2");
+    if (Nb.l_min >= 0) cpy(Nb.G[0], in, blk * 4, st, err);
+    xb_back(x, st);
+    reduce_out();
+  } else {
+    CFG(in && in2 && out && out2, "phase 3: in / in2 = summed g_lik / sum r^2, out / out2 = grad / logp");
+    cpy(x->gl, in, Ck * 4, st, err);
+    cpy(x->lik, in2, (size_t)x->C * 8, st, err);
+    k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), 0);
+    cpy(out, x->wrk_grad, Ck * 4, st, err);
+    cpy(out2, x->wrk_logp, (size_t)x->C * 8, st, err);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  API_END
+}
+
+// Test hook: the POINTS_XB permutations alone: dir 0 = k_xb_gather ([rank][chain][i][k] ->
+// [chain][rank n_loc + i][k]), dir 1 = k_xb_scatter (the inverse); device pointers, synchronous.
+int hmc_debug_xb_permute(int32_t dir, int32_t C, int32_t G, int64_t n_loc, int32_t p, const float* in, float* out,
+                         void* stream) {
+  if (!in || !out || C < 1 || G < 1 || n_loc < 1 || p < 1 || (dir != 0 && dir != 1)) {
+    g_err = "config: in / out non-NULL, C, G, n_loc, p >= 1, dir 0 or 1";
+    return HMC_E_CONFIG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dir == 0) k_xb_gather<<<148 * 4, 256, 0, st>>>(in, out, C, G, n_loc, p);
+  else k_xb_scatter<<<148 * 4, 256, 0, st>>>(in, out, C, G, n_loc, p);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { g_err = cudaGetErrorString(e); return HMC_E_CUDA; }
+  return HMC_OK;
 }
 
 int hmc_debug_set_engine(int32_t mode) {

@@ -42,20 +42,22 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(abi.hmc_net) == 32
     assert abi.hmc_arch.net.offset == 8
     assert ctypes.sizeof(abi.hmc_data) == 10 * 8 and abi.hmc_data.q_per_pair.offset == 9 * 8
-    assert abi.hmc_config.nccl_id.offset == ctypes.sizeof(abi.hmc_config) - 8
+    assert abi.hmc_config.exchange.offset == abi.hmc_config.nccl_id.offset + 8
+    assert ctypes.sizeof(abi.hmc_config) == abi.hmc_config.exchange.offset + 8
 
 
 def test_c_struct_sizes_via_compiler(tmp_path):
     """Compile a tiny C program against include/hmc.h and compare sizeof/offsetof with ctypes."""
     from paper_2507_14652_b200 import abi
     c = tmp_path / "s.c"
-    c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hmc.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n",'
-                 'sizeof(hmc_net),sizeof(hmc_arch),sizeof(hmc_data),sizeof(hmc_config),offsetof(hmc_config,seed));}\n')
+    c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hmc.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
+                 'sizeof(hmc_net),sizeof(hmc_arch),sizeof(hmc_data),sizeof(hmc_config),offsetof(hmc_config,seed),'
+                 'offsetof(hmc_config,exchange));}\n')
     exe = tmp_path / "s"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
     vals = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     assert vals == [ctypes.sizeof(abi.hmc_net), ctypes.sizeof(abi.hmc_arch), ctypes.sizeof(abi.hmc_data),
-                    ctypes.sizeof(abi.hmc_config), abi.hmc_config.seed.offset]
+                    ctypes.sizeof(abi.hmc_config), abi.hmc_config.seed.offset, abi.hmc_config.exchange.offset]
 
 
 def test_product_path_does_not_import_oracle():
