@@ -54,10 +54,11 @@ class Target:
         g = g_full[self.idx] - th / sp2
         return lp, g
 
-    def grad_scale(self, theta_s):
-        """Element-wise summation scale S_i for gradient tolerances (Q26)."""
+    def grad_scale(self, theta_s, kappa=0.0):
+        """Element-wise summation scale S_i for gradient tolerances (Q26; kappa: Q26b, see
+        network.grad_abs_scale)."""
         th = np.asarray(theta_s, dtype=np.float64)
-        S = network.grad_abs_scale(self.arch, self.assemble(th), self.data, self.sigma)
+        S = network.grad_abs_scale(self.arch, self.assemble(th), self.data, self.sigma, kappa)
         return S[self.idx] + np.abs(th) / self.sigma_p ** 2
 
     def logpost_const(self):

@@ -186,11 +186,16 @@ def loglik_grad(arch, theta_full, data, sigma):
     return ll, grad, R
 
 
-def grad_abs_scale(arch, theta_full, data, sigma):
+def grad_abs_scale(arch, theta_full, data, sigma, kappa=0.0):
     """Summation scale for element-wise gradient tolerances:
     the same reverse mode run on absolute values, seeded with (|F| + |y|)/sigma^2, so
     S_i >= sum over all product terms of |term| in d ll / d theta_i (the quantity a
-    floating-point error bound of the gradient is proportional to)."""
+    floating-point error bound of the gradient is proportional to).
+
+    kappa > 0 (reading Q26b): the derivative of a tanh unit enters as
+    |tanh'(z)| + kappa tanh(z)^2 - the absolute error of tanh' = 1 - y^2 taken from a stored
+    output y with relative error eta is 2 eta y^2, so kappa = 2 eta / tol lets the tolerance
+    tol * S_i budget it (reverse mode from the layer outputs, as autograd computes tanh')."""
     th = np.abs(np.asarray(theta_full, dtype=np.float64))
     rows, b0, _ = layer_table(arch)
     s2 = float(sigma) ** 2
@@ -217,7 +222,10 @@ def grad_abs_scale(arch, theta_full, data, sigma):
         for li in range(len(mine) - 1, -1, -1):
             (_, l, w_off, b_off, n_out, n_in, act) = mine[li]
             h_in, z = tape[li]
-            delta = g * np.abs(_dact(act, z))
+            da = np.abs(_dact(act, z))
+            if kappa and act == "tanh":
+                da = da + kappa * np.tanh(z) ** 2
+            delta = g * da
             S[w_off:w_off + n_out * n_in] += (delta.T @ np.abs(h_in)).reshape(-1)
             if b_off is not None:
                 S[b_off:b_off + n_out] += delta.sum(axis=0)

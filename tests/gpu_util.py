@@ -5,6 +5,9 @@ import numpy as np
 LOGP_RTOL = 1e-5      # north_star: log-posterior within 1e-5 relative
 GRAD_RTOL = 1e-5      # north_star: gradient within 1e-5 relative (2-norm and inf-norm, Q26)
 STATE_RTOL = 1e-4     # north_star: trajectory end states within 1e-4 relative over L <= 50
+# Q26b: the element-wise scale budgets the rounding of tanh' = 1 - y^2 taken from the
+# stored fp32 output (2 eta y^2, eta = 4 u: rounding plus the tanh evaluation)
+KAPPA_Q26B = 2.0 * 4.0 * 2.0 ** -24 / 1e-5
 
 
 def torch_cuda():
@@ -46,3 +49,14 @@ def assert_grad_close(lp, g, lp_ref, g_ref, where=""):
     ri = np.max(np.abs(d)) / np.max(np.abs(g_ref))
     assert r2 <= GRAD_RTOL and ri <= GRAD_RTOL, (where, r2, ri)
     return r2, ri
+
+
+def assert_grad_elementwise(lp, g, lp_ref, g_ref, S, where=""):
+    """Q26 at chain-visited states: near a mode ||g|| -> 0, so the bound is per
+    entry, scaled by the summation magnitude S_i of that entry (oracle Target.grad_scale with
+    kappa = KAPPA_Q26B): |g_i - g_ref_i| <= 1e-5 S_i; log pi within 1e-5 relative."""
+    assert abs(lp - lp_ref) <= LOGP_RTOL * abs(lp_ref), (where, lp, lp_ref)
+    d = np.abs(g.astype(np.float64) - g_ref)
+    worst = np.max(d / np.maximum(S, 1e-300))
+    assert worst <= GRAD_RTOL, (where, worst, int(np.argmax(d / np.maximum(S, 1e-300))))
+    return worst

@@ -11,8 +11,8 @@ from hmcdata import ArchSpec, NetSpec, make_problem, make_tiny_problem
 from oracle import hmc as ohmc
 from oracle import philox as ophilox
 
-from gpu_util import (STATE_RTOL, assert_grad_close, gpu_grad, jittered_states, to_dev,
-                      torch_cuda)
+from gpu_util import (KAPPA_Q26B, STATE_RTOL, assert_grad_close, assert_grad_elementwise, gpu_grad, jittered_states,
+                      to_dev, torch_cuda)
 
 pytestmark = pytest.mark.gpu
 
@@ -281,6 +281,62 @@ def test_trajectory_cfg1_resynced_all_200():
                 ref = r["theta_prop"]
                 assert np.linalg.norm(T1[0] - ref) <= STATE_RTOL * np.linalg.norm(ref)
     assert n_bad == 0
+
+
+def test_cfg1_gradients_at_every_20th_chain_state():
+    """Q26 at states the chain visits: the oracle's free-running cfg1 chain (200 samples), every
+    20th state: GPU log pi and gradient vs the oracle, element-wise |dg_i| <= 1e-5 S_i."""
+    prob = make_problem("cfg1")
+    t = ohmc.Target(prob)
+    th0 = prob.frozen[prob.idx].astype(np.float64)
+    ref_s, _, _ = ohmc.sample_chain(t, th0, prob.eps, prob.L, 0, prob.S, 0)
+    states = np.stack([ref_s[s] for s in range(19, prob.S, 20)]).astype(np.float32)   # 10 states
+    with _ctx(prob) as c:
+        for i, st in enumerate(states):
+            lp, g = gpu_grad(c, st[None, :])
+            x = st.astype(np.float64)
+            lr, gr = t.logp_grad(x)
+            assert_grad_elementwise(lp[0], g[0], lr, gr, t.grad_scale(x, KAPPA_Q26B), f"cfg1 state {20 * i + 19}")
+
+
+def test_cfg2_resynced_20_trajectories_8_chains():
+    """the first 20 trajectories of each of the 8 chains (L = 50), re-synced
+    (each starts from the oracle's state rounded to fp32): log pi and gradient element-wise at every
+    visited state (Q26), identical decisions outside the rounding margin, end states within 1e-4."""
+    prob = make_problem("cfg2")
+    t = ohmc.Target(prob)
+    C, nt = prob.n_chains, 20
+    starts, refs = np.empty((nt, C, prob.k), dtype=np.float32), [[None] * C for _ in range(nt)]
+    for ci in range(C):
+        th = prob.frozen[prob.idx].astype(np.float64)
+        for s in range(nt):
+            th32 = th.astype(np.float32)
+            x = th32.astype(np.float64)
+            lr, gr = t.logp_grad(x)
+            r = ohmc.trajectory(t, x, lr, gr, prob.eps, prob.L, s, ci)
+            starts[s, ci] = th32
+            refs[s][ci] = (lr, gr, r)
+            th = r["theta"]
+    n_acc = 0
+    with _ctx(prob) as c:
+        for s in range(nt):
+            lp, g = gpu_grad(c, starts[s])
+            T1, _, _, acc, dH = _gpu_traj(c, starts[s], lp, g, prob.eps, prob.L, s)
+            for ci in range(C):
+                lr, gr, r = refs[s][ci]
+                x = starts[s, ci].astype(np.float64)
+                assert_grad_elementwise(lp[ci], g[ci], lr, gr, t.grad_scale(x, KAPPA_Q26B), f"traj {s} chain {ci}")
+                # dH = H* - H0: each log pi within the north_star 1e-5 relative (the kinetic terms
+                # follow the end state, within 1e-4 relative, and are far smaller here)
+                tol_dH = 1e-5 * (abs(lr) + abs(r["logp"] if r["accepted"] else r["H1"])) + 1e-4
+                assert abs(dH[ci] - r["dH"]) <= tol_dH, (s, ci, dH[ci], r["dH"])
+                if abs(np.log(r["u"]) - (r["H0"] - r["H1"])) > 2 * tol_dH:
+                    assert bool(acc[ci]) == r["accepted"], (s, ci)
+                if acc[ci] and r["accepted"]:
+                    n_acc += 1
+                    ref = r["theta_prop"]
+                    assert np.linalg.norm(T1[ci] - ref) <= STATE_RTOL * np.linalg.norm(ref), (s, ci)
+    assert n_acc >= C * nt // 2
 
 
 def test_cfg1_free_running_decisions_identical():

@@ -10,9 +10,10 @@ from gpu_util import torch_cuda
 
 pytestmark = pytest.mark.gpu
 
-# fp32 sums of squares over the data (3xTF32 or FMA): relative error ~1e-6 per entry
-REL2 = 2e-5      # ||S2_gpu - S2_ref|| / ||S2_ref||
-RELI = 2e-4      # per entry, relative to the entry, for entries >= 1e-4 max
+# fp32 sums of squares over the data (3xTF32 or FMA): relative error ~1e-6 per entry; the
+# north_star tolerance (1e-5) on the norm and on every entry that is not ~1e3 times below the max
+REL2 = 1e-5      # ||S2_gpu - S2_ref|| / ||S2_ref||
+RELI = 1e-5      # per entry, relative to the entry, for entries >= 1e-3 max
 
 
 def _data(prob):
@@ -30,18 +31,31 @@ def _check(prob):
     assert got.shape == ref.shape and np.all(got >= 0)
     r2 = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert r2 <= REL2, r2
-    big = ref >= 1e-4 * ref.max()
+    big = ref >= 1e-3 * ref.max()
     ri = np.max(np.abs(got[big] - ref[big]) / ref[big])
     assert ri <= RELI, ri
-    # the partition the paper's Algorithm 2 builds from them (tau = 0.9): same N^, and the same
-    # sets unless scores are within rounding of each other at the cut
+    # the partition the paper's Algorithm 2 builds from them: bit-exact (same N^, same index set)
+    # whenever the oracle's own margins at the cut exceed the measured error - the gap between the
+    # last selected and the first unselected score, and the distance of the cumulative fractions
+    # c_{N^-1}, c_{N^} from tau; otherwise (a cut inside the rounding band) N^ within 1
+    err = np.abs(got - ref)
+    n_exact = 0
     for tau in (0.5, 0.9, 0.99):
-        n_g, n_r = osens.n_hat(got, tau), osens.n_hat(ref, tau)
-        assert abs(n_g - n_r) <= 1, (tau, n_g, n_r)
-        a_g = set(osens.partition(got, tau)[0].tolist())
-        a_r = set(osens.partition(ref, tau)[0].tolist())
-        assert len(a_g ^ a_r) <= 2, (tau, len(a_g ^ a_r))
-    return got, ref
+        n_r = osens.n_hat(ref, tau)
+        order = np.lexsort((np.arange(ref.size), -ref))
+        srt = ref[order]
+        csum = np.cumsum(srt) / srt.sum()
+        e_tot = err.sum() / srt.sum()
+        gap_ok = n_r >= srt.size or (srt[n_r - 1] - srt[n_r]) > err[order[n_r - 1]] + err[order[n_r]]
+        c_ok = abs(csum[n_r - 1] - tau) > 2 * e_tot and (n_r < 2 or abs(csum[n_r - 2] - tau) > 2 * e_tot)
+        n_g = osens.n_hat(got, tau)
+        if gap_ok and c_ok:
+            n_exact += 1
+            assert n_g == n_r, (tau, n_g, n_r)
+            np.testing.assert_array_equal(osens.partition(got, tau)[0], osens.partition(ref, tau)[0])
+        else:
+            assert abs(n_g - n_r) <= 1, (tau, n_g, n_r)
+    return got, ref, n_exact
 
 
 CASES = {
@@ -64,8 +78,12 @@ def test_sensitivity_matches_oracle(name):
 
 
 def test_sensitivity_cfg2_full_size():
-    """cfg2 (MLP 1-64x4-1, N = 1024) at full size."""
-    _check(make_problem("cfg2", n_chains=1))
+    """cfg2 (MLP 1-64x4-1, N = 1024) at full size; its cuts at tau = 0.5 and 0.9 lie 1e-3 / 8e-4
+    (score gap) and 1.3e-3 / 1.8e-5 (cumulative fraction) away from any tie, far outside the
+    ~1e-6 rounding band, so those partitions must be bit-exact (tau = 0.99's cut is 7e-7 from
+    c_{N^-1} and may legitimately move by one)."""
+    _, _, n_exact = _check(make_problem("cfg2", n_chains=1))
+    assert n_exact >= 2
 
 
 def test_sensitivity_cfg4_shape_deeponet():
@@ -75,7 +93,7 @@ def test_sensitivity_cfg4_shape_deeponet():
     full.u = np.ascontiguousarray(full.u[:24])
     full.q = np.ascontiguousarray(full.q[:30])
     full.v = np.ascontiguousarray(full.v[:24, :30])
-    got, ref = _check(full)
+    got, ref, _ = _check(full)
     b0 = full.frozen.shape[0] - 1
     assert got[b0] == pytest.approx(float(full.sigma_vi[b0]) ** 2, rel=1e-6)   # dF/db0 = 1
 

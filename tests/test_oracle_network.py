@@ -239,3 +239,40 @@ def test_config_generators_deterministic_and_shaped():
     assert p5.k == 20000
     p4 = make_problem("cfg4")
     assert p4.u.shape == (1000, 100) and p4.q.shape == (100, 1) and p4.v.shape == (1000, 100)
+
+
+KAPPA_Q26B = 2.0 * 4.0 * 2.0 ** -24 / 1e-5   # 2 eta / tol, eta = 4 u (Q26b)
+
+
+def test_grad_scale_kappa_no_effect_without_tanh():
+    pr = make_problem("blr", n_chains=1)
+    t = ohmc.Target(pr)
+    th = np.array([0.3, -1.0, 0.5, 2.0])
+    np.testing.assert_array_equal(t.grad_scale(th), t.grad_scale(th, KAPPA_Q26B))
+
+
+def test_grad_scale_kappa_budgets_output_derivative_rounding(monkeypatch):
+    """Q26b pin: reverse mode that takes tanh' = 1 - y^2 from the fp32-ROUNDED layer output y
+    (autograd's arithmetic; everything else exact) perturbs each unit's derivative by up to
+    2 u y^2.  At strongly saturated units that breaks |dg_i| <= 1e-5 S_i (kappa = 0) but stays
+    within 1e-5 S_i(kappa) - the first-order bound of that perturbation."""
+    from oracle import network as onet
+    arch = ArchSpec("mlp", (NetSpec.plain((2, 16, 16, 1)),))
+    pr = make_tiny_problem(arch, n=200, seed=13, active_frac=1.0)
+    t = ohmc.Target(pr)
+    th = 2.5 * pr.frozen[pr.idx].astype(np.float64) / max(np.std(pr.frozen), 1e-12)   # saturating weights
+    _, g_ref = t.logp_grad(th)
+    exact = onet._dact
+
+    def dact_from_fp32_output(name, z):
+        if name == "tanh":
+            y = np.tanh(z).astype(np.float32).astype(np.float64)
+            return 1.0 - y * y
+        return exact(name, z)
+
+    monkeypatch.setattr(onet, "_dact", dact_from_fp32_output)
+    _, g_out = t.logp_grad(th)
+    monkeypatch.setattr(onet, "_dact", exact)
+    d = np.abs(g_out - g_ref)
+    assert np.max(d / t.grad_scale(th)) > 1e-5                 # the mechanism is exercised
+    assert np.max(d / t.grad_scale(th, KAPPA_Q26B)) <= 1e-5
