@@ -178,6 +178,8 @@ DATA_SHARD = {"cfg3": "rows", "cfg5": "points_xb"}
 
 
 def _parallel(args, world):
+    if args.parallel == "data":          # (also at N = 1: the DATA-mode code path over a communicator of one)
+        return "data", DATA_SHARD.get(args.cfg, "rows")
     if world == 1:
         return "single", None
     if args.parallel == "chain" or (args.parallel == "auto" and args.cfg not in DATA_SHARD):
@@ -415,11 +417,11 @@ def run_ours(args):
            "body_flops_per_eval_all_chains": body_flops,
            "gpu_launches": launches, "roofline": roofline, "whole_eval": whole, "cpu_baseline": cpu,
            "e2e": e2e, "clocks": clocks}
-    if rank == 0:
-        print(json.dumps(out), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:   # last: after NCCL's teardown messages (NCCL_DEBUG=INFO prints to stdout)
+        print(json.dumps(out), flush=True)
 
 
 # F_eval = 6 N P (MLP) or 6 (N_c P_b + N_x P_t) + 6 N_c N_x p (factored DeepONet)

@@ -529,58 +529,69 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
   if (ov) cudaStreamWaitEvent(ms, N.evW[N.l_min], 0);  // all weight gradients done (stream order)
 }
 
-// POINTS_XB after the all-gather of the branch outputs (xb_recv, [rank][chain][i][k]): order them
-// per chain, combine with this rank's points (residual and likelihood partials), the partial dB
-// over these points for all conditions, ordered for the reduce-scatter (xb_send)
-void xb_mid(hmc_ctx* x, cudaStream_t st) {
-  const int C = x->C;
-  NetInfo& Nb = x->nets[0];
-  const LayerInfo& Bl = x->layers[Nb.layers.back()];
-  const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
-  const int p = Bl.n_out;
-  k_xb_gather<<<148 * 4, 256, 0, st>>>(x->xb_recv, x->xb_full, C, x->world, x->n_c_loc, p);
+// POINTS_XB pieces: the all-gather result xb_recv ([rank][chain][i][k]) ordered
+// per chain into xb_full; the combine of all conditions with this rank's points (residual and
+// likelihood partials); the partial dB over these points for all conditions, ordered for the
+// reduce-scatter (xb_send); dT = R^T B_all (complete locally)
+void xb_gather_perm(hmc_ctx* x, cudaStream_t st) {
+  const int p = x->layers[x->nets[0].layers.back()].n_out;
+  k_xb_gather<<<148 * 4, 256, 0, st>>>(x->xb_recv, x->xb_full, x->C, x->world, x->n_c_loc, p);
   x->launches++;
-  {
-    GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, C);
-    a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
-    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-    a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
-    a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
-    if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
-    a.inv_s2 = 1.0 / (x->sigma * x->sigma);
-    a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
-    launch_gemm(x, a, true, true, st, "combine");
-  }
-  if (Nb.l_min >= 0) {  // partial dB over this rank's points, all conditions, then the send order
-    GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
-    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
-    a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-    a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
-    a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
-    launch_gemm(x, a, true, false, st, "dB");
-    k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, C, x->world, x->n_c_loc, p);
-    x->launches++;
-  }
 }
 
-// POINTS_XB after the reduce-scatter of dB into the branch's gradient buffer: dT = R^T B_all
-// (complete locally), then both nets' backward
-void xb_back(hmc_ctx* x, cudaStream_t st) {
-  const int C = x->C;
-  NetInfo& Nb = x->nets[0];
+void xb_combine(hmc_ctx* x, cudaStream_t st) {
+  const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
+  const int p = Tl.n_out;
+  GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, x->C);
+  a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
+  a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+  a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
+  a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
+  if (x->has_b0) { a.b0 = x->Wd + x->b0_off; a.s_b0 = x->P; }
+  a.inv_s2 = 1.0 / (x->sigma * x->sigma);
+  a.part_sq = x->part_sq; a.part_r = x->part_r; a.n_part = x->n_part;
+  launch_gemm(x, a, true, true, st, "combine");
+}
+
+void xb_dB(hmc_ctx* x, cudaStream_t st) {
+  const LayerInfo& Bl = x->layers[x->nets[0].layers.back()];
+  const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
+  const int p = Bl.n_out;
+  GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, x->C);
+  a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+  a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
+  a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
+  a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
+  launch_gemm(x, a, true, false, st, "dB");
+  k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, x->C, x->world, x->n_c_loc, p);
+  x->launches++;
+  x->nets[0].cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
+}
+
+void xb_dT(hmc_ctx* x, cudaStream_t st) {
   NetInfo& Nt = x->nets[1];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Tl.n_out;
-  if (Nb.l_min >= 0) Nb.cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
-  if (Nt.l_min >= 0) {
-    GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
-    a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
-    a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
-    a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
-    a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
-    if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
-    Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
-  }
+  GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, x->C);
+  a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
+  a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
+  a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
+  a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
+  if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
+  Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+}
+
+// (single-stream sequences, used by the emulated-exchange phases hmc_debug_data_phase)
+void xb_mid(hmc_ctx* x, cudaStream_t st) {
+  xb_gather_perm(x, st);
+  xb_combine(x, st);
+  if (x->nets[0].l_min >= 0) xb_dB(x, st);
+}
+
+void xb_back(hmc_ctx* x, cudaStream_t st) {
+  NetInfo& Nb = x->nets[0];
+  NetInfo& Nt = x->nets[1];
+  if (Nt.l_min >= 0) xb_dT(x, st);
   if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
   if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
 }
@@ -633,7 +644,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   // (two_streams: the branch net's kernels go to a second captured stream, so the short branch
   // GEMMs fill the trunk GEMMs' last waves; fork / join through events)
   // (the profiled step - prof_armed - runs on one stream, so each kernel is timed alone)
-  const bool two = x->two_streams && !x->xb && !x->unaligned && !x->prof_armed;
+  const bool two = x->two_streams && !x->unaligned && !x->prof_armed;
   cudaStream_t sb = two ? x->st2 : st;
   auto fork = [&](int i) {
     if (!two) return;
@@ -645,25 +656,42 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     cudaEventRecord(x->ev_join[i], sb);
     cudaStreamWaitEvent(st, x->ev_join[i], 0);
   };
-  fork(0);
-  for (int i = 0; i < (int)x->nets[0].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[0], i, sb);
-  for (int i = 0; i < (int)x->nets[1].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[1], i, st);
-  join(0);
   NetInfo& Nb = x->nets[0];
   NetInfo& Nt = x->nets[1];
   const LayerInfo& Bl = x->layers[Nb.layers.back()];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Bl.n_out;
   if (x->xb) {  // POINTS_XB: gather the branch outputs of all conditions, combine with this rank's
-                // points, reduce-scatter dB back to the condition owners, dT stays local
+                // points, reduce-scatter dB back to the condition owners, dT stays local.  The
+                // exchanges run on the branch stream: the all-gather overlaps the trunk forward,
+                // the reduce-scatter (and the branch backward after it) the dT GEMM and the trunk
+                // backward
     std::string& err = x->err;  // (CKN reports through it)
     const int64_t blk = (int64_t)C * x->n_c_loc * p;
-    CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, st));
-    xb_mid(x, st);
-    if (Nb.l_min >= 0) CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, st));
-    xb_back(x, st);
+    fork(0);
+    for (int i = 0; i < (int)Nb.layers.size(); ++i) enqueue_forward_hidden(x, Nb, i, sb);
+    CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, sb));
+    xb_gather_perm(x, sb);
+    for (int i = 0; i < (int)Nt.layers.size(); ++i) enqueue_forward_hidden(x, Nt, i, st);
+    join(0);
+    xb_combine(x, st);
+    fork(1);
+    if (Nb.l_min >= 0) {
+      xb_dB(x, sb);
+      CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, sb));
+      enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, sb);
+    }
+    if (Nt.l_min >= 0) {
+      xb_dT(x, st);
+      enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    }
+    join(1);
     return;
   }
+  fork(0);
+  for (int i = 0; i < (int)x->nets[0].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[0], i, sb);
+  for (int i = 0; i < (int)x->nets[1].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[1], i, st);
+  join(0);
   if (x->unaligned) {  // per-pair trunk rows: row-wise combine, then the two output gradients
     k_pair_combine<<<dim3((unsigned)x->n_c, C), 256, p * sizeof(float), st>>>(
         Bl.A, Tl.A, p, x->n_c, x->n_x, x->d_v, x->has_b0 ? x->Wd + x->b0_off : nullptr, x->P,
@@ -1267,7 +1295,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->n_c_loc = x->xb ? x->n_c / cfg->world : x->n_c;
     {
       const char* e = dev_env("HMC_STREAMS");
-      x->two_streams = !x->unaligned && !x->xb && !(e && atoi(e) == 1);
+      x->two_streams = !x->unaligned && !(e && atoi(e) == 1);
       x->wgrad_ov = x->two_streams;
     }
     const int64_t q_rows = x->unaligned ? x->n_c * x->n_x : x->n_x;
