@@ -945,7 +945,7 @@ bool nw_layout(hmc_ctx* x, int bpc, int nc, nw::NarrowArgs& a) {
 // CTA bpc (results do not depend on them): the feasible (shared memory, co-resident cluster)
 // choice with the fewest block-times per chain batch, ceil(C / active clusters) x bpc.
 bool plan_narrow(hmc_ctx* x, std::string& err) {
-  if (x->kind != HMC_MLP || x->mode == HMC_MODE_DATA || engine_override() != 0) return false;
+  if (x->kind != HMC_MLP || x->mode == HMC_MODE_DATA || (engine_override() != 0 && engine_override() != 3)) return false;
   const NetInfo& N = x->nets[0];
   const int nl = (int)N.layers.size();
   if (nl > nw::MAXL || N.l_min < 0) return false;
@@ -1010,6 +1010,32 @@ bool plan_narrow(hmc_ctx* x, std::string& err) {
       x->nw_clusters = clusters;
     }
   }
+  // grid mode: every CTA of every chain resident at once (cooperative launch), any nc up to nblk,
+  // exchanges through L2 - chosen when it needs fewer block-times than the best cluster shape
+  // (clusters of 16 are limited by the GPC layout: 7 co-resident at 1 CTA per SM on B200)
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  for (int nc = std::min(a.nblk, nsm); nc >= 1 && engine_override() != 3; --nc) {
+    const int bpc = (a.nblk + nc - 1) / nc;
+    if ((nc - 1) * bpc >= a.nblk) continue;
+    nw::NarrowArgs t = a;
+    nw_layout(x, bpc, nc, t);
+    if (t.smem_bytes > optin) continue;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw::NT, t.smem_bytes));
+    if ((int64_t)x->C * nc > (int64_t)per_sm * nsm) continue;
+    const double cost = (double)bpc;
+    if (cost < best - 1e-9) {
+      best = cost;
+      t.nc = nc;
+      t.grid = 1;
+      x->nwa = t;
+      x->nw_hw = hw;
+      x->nw_clusters = 0;
+    }
+    break;  // (the largest feasible nc has the fewest blocks per CTA)
+  }
   if (best >= 1e30) return false;
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x->nwa.smem_bytes));
   return true;
@@ -1029,10 +1055,16 @@ void launch_narrow(hmc_ctx* x, int nsteps, int last_mode, cudaStream_t st, std::
   cfg.dynamicSmemBytes = a.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = a.nc;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
+  if (a.grid) {  // every CTA resident (the per-chain barriers spin on each other)
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    CK(cudaMemsetAsync(a.xbar, 0, (size_t)x->C * sizeof(unsigned), st));
+  } else {
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = a.nc;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+  }
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   KState ks = x->kstate();
@@ -1447,6 +1479,13 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       }
     x->d_soff = dalloc<int32_t>(x, x->k, err);
     CK(cudaMemcpy(x->d_soff, soff.data(), x->k * 4, cudaMemcpyHostToDevice));
+    if (x->nwa.grid) {  // L2 exchange buffers of the grid mode
+      nw::NarrowArgs& a = x->nwa;
+      a.xpart = dalloc<float>(x, (size_t)x->C * a.nc * a.nblk * a.ksp, err);
+      a.xtheta = dalloc<float>(x, (size_t)x->C * x->k, err);
+      a.xsq = dalloc<double>(x, (size_t)x->C * a.nblk, err);
+      a.xbar = dalloc<unsigned>(x, (size_t)x->C, err);
+    }
   }
   for (int c = 0; c < C; ++c) CK(cudaMemcpy(x->Wd + (size_t)c * x->P, h_frozen.data(), x->P * 4, cudaMemcpyHostToDevice));
   if (x->Ptc > 0) {
@@ -1599,7 +1638,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     }
     CKN(ncclCommInitRank(&x->comm, x->world, id, x->rank));
   }
-  x->engine = x->narrow ? "narrow-simt (cluster " + std::to_string(x->nwa.nc) + " x " + std::to_string(x->nwa.bpc) +
+  x->engine = x->narrow ? std::string("narrow-simt (") + (x->nwa.grid ? "grid " : "cluster ") + std::to_string(x->nwa.nc) + " x " + std::to_string(x->nwa.bpc) +
                               " blocks of " + std::to_string(x->nwa.rb) + " rows, " + std::to_string(x->nwa.nblk) +
                               " blocks, hw " + std::to_string(x->nw_hw) + ")"
                         : x->tc.describe();
@@ -2168,8 +2207,9 @@ int hmc_debug_xb_permute(int32_t dir, int32_t C, int32_t G, int64_t n_loc, int32
 }
 
 int hmc_debug_set_engine(int32_t mode) {
-  if (mode < 0 || mode > 2) {
-    g_err = "config: engine mode must be 0 (automatic), 1 (per-layer SIMT only) or 2 (per-layer engines)";
+  if (mode < 0 || mode > 3) {
+    g_err = "config: engine mode must be 0 (automatic), 1 (per-layer SIMT only), 2 (per-layer engines) or 3 "
+            "(narrow engine in cluster mode only)";
     return HMC_E_CONFIG;
   }
   engine_override() = mode;

@@ -57,6 +57,14 @@ struct NarrowArgs {
   int s_y;                    // this CTA's targets y [rows]
   int s_slot;                 // the slot map [P], resident: int16 when k < 32768 (slot16), else int32
   int slot16;
+  // grid mode (cooperative launch, every CTA resident; used when a chain's CTAs cannot all be
+  // co-resident clusters): the exchanges go through L2 instead of distributed shared memory and
+  // the barriers are per-chain counters
+  int grid;
+  float* xpart;               // [C][nc][nblk][ksp] block partials, by owner slice
+  float* xtheta;              // [C][k] the new theta of the step
+  double* xsq;                // [C][nblk] sum r^2 per block
+  unsigned* xbar;             // [C] barrier counters (zeroed before every launch)
   int dbg;                    // dev experiments (HMC_NW_DBG, -DHMC_DEV only): bit 0 skip weight-gradient
                               // FMAs, 1 skip input-gradient GEMMs, 2 skip forward GEMMs (results wrong)
   int s_red;                  // offset (floats, 8-byte aligned) of the fp64 reduction slots
@@ -148,6 +156,20 @@ __device__ unsigned long long g_nwprof[10];
 #else
 #define NW_T(i)
 #endif
+
+// grid mode: barrier of the nc CTAs of one chain (monotonic counter; target = nc x barrier count)
+__device__ __forceinline__ void chain_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ float nw_act(int act, float z) { return act == ACT_TANH ? tanh_acc(z) : z; }
 __device__ __forceinline__ float nw_dact(int act, float a) { return act == ACT_TANH ? fmaf(-a, a, 1.f) : 1.f; }
@@ -424,7 +446,12 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
   extern __shared__ __align__(16) float sm[];
   const int nc = a.nc;
   const int c = blockIdx.x / nc;
-  const uint32_t rank = rank_in_cluster();
+  const uint32_t rank = a.grid ? (uint32_t)(blockIdx.x % nc) : rank_in_cluster();
+  unsigned nbar = 0;  // grid mode: barriers passed
+  auto sync_chain = [&]() {
+    if (a.grid) chain_barrier(a.xbar + c, (unsigned)nc * ++nbar);
+    else cluster_barrier();
+  };
   const int tid = threadIdx.x;
   const int rows = a.bpc * a.rb;                       // rows of this CTA (blocks rank*bpc ..)
   const int64_t row0 = (int64_t)rank * rows;
@@ -538,6 +565,7 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
         double sq = 0.0;
         for (int r = tid * a.rb; r < (tid + 1) * a.rb; ++r) sq += (double)Rr[r] * (double)Rr[r];
         red[tid] = sq;
+        if (a.grid) __stcg(a.xsq + (int64_t)c * a.nblk + rank * a.bpc + tid, sq);
       }
       // output-layer weight / bias gradient of each block: dw[i] = sum_r R[r] A[r][i], db = sum_r R[r]
       // (one thread per (block, input), rows in order)
@@ -606,19 +634,27 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
       for (int t = tid; t < nb * nc * nv; t += NT) {
         const int b = t / (nc * nv), rem = t - b * nc * nv, q = rem / nv, u = rem - q * nv;
         const float4 v = *reinterpret_cast<const float4*>(gp + b * a.kp + q * a.ksp + 4 * u);
-        st_cluster4(map_cta(recv_addr + 4u * (uint32_t)(((int)rank * a.bpc + b) * a.ksp + 4 * u), (uint32_t)q), v);
+        const int gb = (int)rank * a.bpc + b;
+        if (a.grid)
+          __stcg(reinterpret_cast<float4*>(a.xpart + (((int64_t)c * nc + q) * a.nblk + gb) * a.ksp + 4 * u), v);
+        else
+          st_cluster4(map_cta(recv_addr + 4u * (uint32_t)(gb * a.ksp + 4 * u), (uint32_t)q), v);
       }
     }
     NW_T(2)
-    // ---- cluster barrier 1: every block's partial gradient and sum r^2 are complete ----
-    cluster_barrier();
+    // ---- barrier 1: every block's partial gradient and sum r^2 are complete ----
+    sync_chain();
     NW_T(3)
     // ---- k-slice reduction over the row blocks (block order), prior, kick / drift ----
-    double th2 = 0.0;
     for (int64_t j = j_lo + tid; j < j_hi; j += NT) {
       // the pushed block partials of entry j, summed in block order
       float gs = 0.f;
-      for (int b = 0; b < a.nblk; ++b) gs += recv[b * a.ksp + (j - j_lo)];
+      if (a.grid) {
+        const float* src = a.xpart + ((int64_t)c * nc + rank) * a.nblk * a.ksp + (j - j_lo);
+        for (int b = 0; b < a.nblk; ++b) gs += __ldcg(src + (int64_t)b * a.ksp);
+      } else {
+        for (int b = 0; b < a.nblk; ++b) gs += recv[b * a.ksp + (j - j_lo)];
+      }
       const int64_t t = (int64_t)c * k + j, jj = j - j_lo;
       float th = sth[jj];
       const float g = gs - (float)((double)th * s.inv_sp2);
@@ -629,14 +665,17 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
         th = fmaf(fe * im, p, th);
         sth[jj] = th;
         if (step + 1 < nsteps) {  // the new weight, into every CTA's resident copy
-          const uint32_t wa = smem_u32(sm + __ldg(a.soff + j));
-          for (int q = 0; q < nc; ++q) st_cluster(map_cta(wa, q), th);
+          if (a.grid) {
+            __stcg(a.xtheta + t, th);
+          } else {
+            const uint32_t wa = smem_u32(sm + __ldg(a.soff + j));
+            for (int q = 0; q < nc; ++q) st_cluster(map_cta(wa, q), th);
+          }
         } else {                  // (a later launch reloads the weights from HBM)
           s.Wd[(int64_t)c * s.P + __ldg(s.idx + j)] = th;
         }
-      } else {
-        if (mode == 2) p = fmaf(fh, g, p);
-        th2 += (double)th * (double)th;
+      } else if (mode == 2) {
+        p = fmaf(fh, g, p);
       }
       spp[jj] = p;
       if (step + 1 == nsteps) {  // the working state the Metropolis kernel reads
@@ -645,22 +684,35 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
         s.wrk_grad[t] = g;
       }
     }
-    if (mode != 1) {  // sum theta^2 of the slice (fixed tree), for log pi
-      th2 = block_sum_d<NT>(th2, scr);
-      if (tid == 0) red[NBMAX] = th2;
-    }
     NW_T(4)
-    // ---- cluster barrier 2: new weights visible everywhere; partials free for the next step ----
-    cluster_barrier();
-    NW_T(5)
-    if (mode != 1 && rank == 0 && tid == 0) {  // log pi, constants dropped (Q7)
-      double sq = 0.0, tt = 0.0;
-      for (int blk = 0; blk < a.nblk; ++blk) sq += ld_cluster_d(map_cta(red_addr + 8u * (uint32_t)(blk % a.bpc), blk / a.bpc));
-      for (int q = 0; q < nc; ++q) tt += ld_cluster_d(map_cta(red_addr + 8u * NBMAX, q));
-      s.wrk_logp[c] = -sq * s.inv_2s2 - 0.5 * tt * s.inv_sp2;
-      const_cast<double*>(s.lik)[c] = sq;
+    // ---- barrier 2: new weights visible everywhere; partials free for the next step ----
+    sync_chain();
+    if (a.grid && mode == 1 && step + 1 < nsteps) {  // the chain's new theta into this CTA's weights
+      for (int64_t j = tid; j < k; j += NT) sm[__ldg(a.soff + j)] = __ldcg(a.xtheta + (int64_t)c * k + j);
+      __syncthreads();
     }
-    if (mode != 1) cluster_barrier();  // (the leader's remote reads finish before any CTA exits)
+    NW_T(5)
+    if (mode != 1 && rank == 0) {  // log pi, constants dropped (Q7): the chain's sum
+                                   // theta^2 over the final working state (fixed tree over k, the same
+                                   // for any nc), sum r^2 over the row blocks in block order
+      double th2 = 0.0;
+      for (int64_t j = tid; j < k; j += NT) {
+        const double v = (double)__ldcg(s.wrk_theta + (int64_t)c * k + j);
+        th2 += v * v;
+      }
+      th2 = block_sum_d<NT>(th2, scr);
+      if (tid == 0) {
+        double sq = 0.0;
+        if (a.grid) {
+          for (int blk = 0; blk < a.nblk; ++blk) sq += __ldcg(a.xsq + (int64_t)c * a.nblk + blk);
+        } else {
+          for (int blk = 0; blk < a.nblk; ++blk) sq += ld_cluster_d(map_cta(red_addr + 8u * (uint32_t)(blk % a.bpc), blk / a.bpc));
+        }
+        s.wrk_logp[c] = -sq * s.inv_2s2 - 0.5 * th2 * s.inv_sp2;
+        const_cast<double*>(s.lik)[c] = sq;
+      }
+    }
+    if (mode != 1 && !a.grid) cluster_barrier();  // (the leader's remote reads finish before any CTA exits)
     NW_T(6)
   }
 }

@@ -189,3 +189,35 @@ def test_narrow_resume_batch_invariance_and_L0():
     np.testing.assert_array_equal(g1, g[2:3])
     np.testing.assert_array_equal(T1[0], T4[2])
     assert acc1[0] == acc4[2] and dH1[0] == dH4[2]
+
+
+def test_narrow_grid_and_cluster_modes_bitwise_equal():
+    """cfg2's 8 chains do not fit as co-resident 16-CTA clusters (7 per GPU), so the batch runs the
+    grid mode (cooperative launch, 16 CTAs x 2 row blocks, exchanges through L2); a single chain
+    runs 32 CTAs x 1 block, and - forced with hmc_debug_set_engine(3) - one cluster (distributed
+    shared memory).  Every sum over data rows is fixed by the row blocks, so chain 3's gradient,
+    trajectory and decision are bitwise the same in all three."""
+    torch = torch_cuda()
+    from paper_2507_14652_b200 import abi
+    prob = make_problem("cfg2")
+    th = jittered_states(prob, prob.n_chains, scale=0.005)
+    with abi.Context(prob) as c:
+        assert "grid" in _engine(c), _engine(c)
+        lp, g = gpu_grad(c, th)
+        T8, LP8, G8, a8, d8 = _traj(c, th, lp, g, prob.eps, prob.L, 5)
+    one = make_problem("cfg2", n_chains=1)
+    one.chain_ids = np.array([3], dtype=np.uint32)
+    for forced in (0, 3):
+        abi.hmc_debug_set_engine(forced)
+        try:
+            with abi.Context(one) as c:
+                assert ("cluster" if forced else "grid 32") in _engine(c), _engine(c)
+                lp1, g1 = gpu_grad(c, th[3:4])
+                T1, LP1, G1, a1, d1 = _traj(c, th[3:4], lp1, g1, prob.eps, prob.L, 5)
+        finally:
+            abi.hmc_debug_set_engine(0)
+        np.testing.assert_array_equal(lp1, lp[3:4])
+        np.testing.assert_array_equal(g1, g[3:4])
+        np.testing.assert_array_equal(T1[0], T8[3])
+        np.testing.assert_array_equal(G1[0], G8[3])
+        assert a1[0] == a8[3] and d1[0] == d8[3]
