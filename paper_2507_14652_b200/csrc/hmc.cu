@@ -10,6 +10,7 @@
 // A trajectory = momentum + L such steps + Metropolis, captured as ONE CUDA graph.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -29,6 +30,13 @@
 using namespace hmc;
 
 static thread_local std::string g_err;
+
+// NVTX range around every public call (SURVEY §5 tracing; header-only NVTX, a no-op unless a tool
+// such as Nsight Systems is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -1683,6 +1691,7 @@ int hmc_comm_unique_id(uint8_t id_out[128]) {
 }
 
 int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, void* stream, hmc_ctx** out) {
+  NvtxRange nvtx_("hmc_setup");
   (void)stream;
   if (!out) {
     g_err = "out is NULL";
@@ -1701,6 +1710,7 @@ int hmc_setup(const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg,
 }
 
 int hmc_grad(hmc_ctx* ctx, const float* theta, double* logp, float* grad, void* stream) {
+  NvtxRange nvtx_("hmc_grad");
   API_BEGIN(ctx)
   if (ctx->emulated) {
     err = "state: an emulated-exchange context (hmc_config.exchange = 1) runs only hmc_debug_data_phase";
@@ -1731,6 +1741,7 @@ int hmc_logpost_const(const hmc_ctx* ctx, double* c) {
 static int run_traj(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps, int32_t L, int64_t iter0,
                     int32_t S, float* samples, uint8_t* acc, double* dH, void* stream, int adapt = 0,
                     double delta = 0.0, double* eps_bar = nullptr) {
+  NvtxRange nvtx_(adapt ? "hmc_adapt" : (S == 1 ? "hmc_trajectory" : "hmc_sample"));
   API_BEGIN(ctx)
   if (ctx->emulated) {
     err = "state: an emulated-exchange context (hmc_config.exchange = 1) runs only hmc_debug_data_phase";
@@ -1819,6 +1830,7 @@ int hmc_adapt(hmc_ctx* ctx, float* theta, double* logp, float* grad, double eps0
 }
 
 int hmc_predict(hmc_ctx* ctx, const float* samples, int64_t S, double* mean, double* var, void* stream) {
+  NvtxRange nvtx_("hmc_predict");
   API_BEGIN(ctx)
   CFG(samples && mean && var && S >= 1, "samples, mean, var must be non-NULL and S >= 1");
   CFG(ctx->mode != HMC_MODE_DATA || ctx->world == 1, "hmc_predict runs on one rank's data (not DATA mode)");
@@ -1990,6 +2002,7 @@ int hmc_diagnostics(const float* samples, int32_t C, int64_t S, int64_t k, doubl
 
 int hmc_sensitivity(const hmc_arch* arch, const hmc_data* data, const float* mu, const float* sigma_vi,
                     double* s2, void* stream) {
+  NvtxRange nvtx_("hmc_sensitivity");
   if (!arch || !data || !mu || !sigma_vi || !s2) {
     g_err = "config: arch, data, mu, sigma_vi and s2 must be non-NULL";
     return HMC_E_CONFIG;
