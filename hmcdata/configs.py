@@ -5,6 +5,8 @@ Pinning follows SURVEY.md §8 "Config pinning" and the readings Q10-Q24 of
 """
 from __future__ import annotations
 
+import json
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Tuple
 
@@ -94,54 +96,31 @@ class Problem:
         return np.repeat(self.frozen[self.idx][None, :], self.n_chains, axis=0).astype(np.float32)
 
 
-# --- the five BASELINE configs -------------------------------------------
-# name -> dict of knobs; generator in generate.py turns these into a Problem.
-CONFIGS = {
-    "cfg1": dict(
-        cid=1,
-        arch=ArchSpec("mlp", (NetSpec.plain((1, 20, 20, 1)),)),
-        n=64, noise=0.1, prior=1.0, active_frac=None, C=1, L=20, eps=1e-3, S=200,
-        mu="n03",
-    ),
-    "cfg2": dict(
-        cid=2,
-        arch=ArchSpec("mlp", (NetSpec.plain((1, 64, 64, 64, 64, 1)),)),
-        n=1024, noise=0.05, prior=1.0, active_frac=0.10, C=8, L=50, eps=5e-4, S=500,
-        mu="n03",
-    ),
-    "cfg3": dict(
-        cid=3,
-        arch=ArchSpec("mlp", (NetSpec.plain((8, 256, 256, 256, 1)),)),
-        n=16384, noise=0.05, prior=1.0, active_frac=0.05, C=32, L=100, eps=2e-4, S=200,
-        mu="lecun",
-    ),
-    "cfg4": dict(
-        cid=4,
-        arch=ArchSpec(
-            "deeponet",
-            (
-                NetSpec.plain((100, 128, 128, 128, 100), last="identity"),
-                NetSpec.plain((1, 128, 128, 100), last="tanh"),
-            ),
-            has_b0=True,
-        ),
-        n_c=1000, n_x=100, noise=0.01, prior=1.0, active_frac=0.10, C=16, L=100, eps=1e-4,
-        S=20, mu="lecun",
-    ),
-    "cfg5": dict(
-        cid=5,
-        arch=ArchSpec(
-            "deeponet",
-            (
-                NetSpec.plain((5, 256, 256, 256, 256, 256), last="identity"),
-                NetSpec.plain((2, 256, 256, 256, 256, 256), last="tanh"),
-            ),
-            has_b0=True,
-        ),
-        n_c=512, n_x=2048, noise=0.02, prior=1.0, active_count=20000, C=64, L=200,
-        eps=5e-5, S=10, mu="lecun",
-    ),
-}
+# --- the five BASELINE configs (SURVEY §5 "one JSON per BASELINE config") ---
+# configs/cfg{1..5}.json hold every knob, with the readings of unstated fields listed under
+# "assumed"; the generator in generate.py turns a config into a Problem.
+CONFIG_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "configs")
+
+
+def load_config(path_or_name: str) -> dict:
+    """A config JSON (a path, or the name of one of configs/*.json) -> the generator's knobs."""
+    path = path_or_name if path_or_name.endswith(".json") else os.path.join(CONFIG_DIR, path_or_name + ".json")
+    with open(path) as f:
+        d = json.load(f)
+    a = d["arch"]
+    arch = ArchSpec(a["kind"], tuple(NetSpec(tuple(n["widths"]), tuple(n["acts"]), tuple(bool(b) for b in n["bias"]))
+                                     for n in a["nets"]), bool(a.get("has_b0", False)))
+    act = d["active"]
+    out = dict(cid=int(d["cid"]), arch=arch, noise=float(d["noise_sigma"]), prior=float(d["prior_sigma"]),
+               active_frac=None if act == "all" else act.get("frac"), C=int(d["chains"]), L=int(d["L"]),
+               eps=float(d["eps"]), S=int(d["S"]), mu=d["frozen_init"])
+    if act != "all" and "count" in act:
+        out["active_count"] = int(act["count"])
+    out.update({k: int(v) for k, v in d["data"].items()})
+    return out
+
+
+CONFIGS = {name: load_config(name) for name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")}
 
 
 def config_names():

@@ -276,3 +276,21 @@ def test_grad_scale_kappa_budgets_output_derivative_rounding(monkeypatch):
     d = np.abs(g_out - g_ref)
     assert np.max(d / t.grad_scale(th)) > 1e-5                 # the mechanism is exercised
     assert np.max(d / t.grad_scale(th, KAPPA_Q26B)) <= 1e-5
+
+
+def test_config_json_files():
+    """configs/cfg{1..5}.json: every BASELINE config, its unstated fields listed under
+    "assumed" with the reading, and the generator's parameter / mask sizes from them."""
+    import json
+    import os
+    from hmcdata.configs import CONFIG_DIR, load_config
+    want = {"cfg1": (481, 481), "cfg2": (12673, 1267), "cfg3": (134145, 6707), "cfg4": (88521, 8852),
+            "cfg5": (528641, 20000)}
+    for name, (P, k) in want.items():
+        d = json.load(open(os.path.join(CONFIG_DIR, name + ".json")))
+        assert d["name"] == name and "assumed" in d and "seed" in d["assumed"]
+        if name != "cfg1":
+            assert "prior_sigma" in d["assumed"] and "mask" in d["assumed"]
+        assert load_config(name)["cid"] == int(name[-1])
+        p = make_problem(name, n_chains=1)
+        assert (p.P, p.k) == (P, k)
