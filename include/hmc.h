@@ -113,7 +113,11 @@ typedef struct {
   const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode, world > 1) */
   int32_t exchange;     /* DATA mode: 0 = in-graph NCCL collectives (the product path); 1 = test hook,
                            no communicator: the context only runs hmc_debug_data_phase and the caller
-                           performs the cross-rank steps (several ranks emulated on one GPU) */
+                           performs the cross-rank steps (several ranks emulated on one GPU);
+                           2 = timing stand-in, no communicator: the all-gather / reduce-scatter are
+                           replaced by local copies of the same bytes and the all-reduce is skipped,
+                           so one GPU can time one rank's share of a G-rank job (results are NOT
+                           the data-mode posterior; scripts/project_scaling.py) */
 } hmc_config;
 
 typedef struct hmc_ctx hmc_ctx;

@@ -494,7 +494,7 @@ class Context:
         c.mode = MODE[mode]
         c.rank, c.world = int(rank), int(world)
         c.shard = SHARD[shard]
-        c.exchange = {"nccl": 0, "emulated": 1}[exchange]
+        c.exchange = {"nccl": 0, "emulated": 1, "local": 2}[exchange]
         if nccl_id is not None:
             idbuf = (ctypes.c_uint8 * 128)(*nccl_id)
             keep.append(idbuf)

@@ -678,7 +678,12 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     const int64_t blk = (int64_t)C * x->n_c_loc * p;
     fork(0);
     for (int i = 0; i < (int)Nb.layers.size(); ++i) enqueue_forward_hidden(x, Nb, i, sb);
-    CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, sb));
+    if (x->comm) {
+      CKN(ncclAllGather(Bl.A, x->xb_recv, (size_t)blk, ncclFloat32, x->comm, sb));
+    } else {  // exchange = 2 (timing stand-in): the same bytes moved locally
+      for (int r = 0; r < x->world; ++r)
+        CK(cudaMemcpyAsync(x->xb_recv + (size_t)r * blk, Bl.A, (size_t)blk * 4, cudaMemcpyDeviceToDevice, sb));
+    }
     xb_gather_perm(x, sb);
     for (int i = 0; i < (int)Nt.layers.size(); ++i) enqueue_forward_hidden(x, Nt, i, st);
     join(0);
@@ -686,7 +691,10 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     fork(1);
     if (Nb.l_min >= 0) {
       xb_dB(x, sb);
-      CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, sb));
+      if (x->comm)
+        CKN(ncclReduceScatter(x->xb_send, Nb.G[0], (size_t)blk, ncclFloat32, ncclSum, x->comm, sb));
+      else
+        CK(cudaMemcpyAsync(Nb.G[0], x->xb_send + (size_t)x->rank * blk, (size_t)blk * 4, cudaMemcpyDeviceToDevice, sb));
       enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, sb);
     }
     if (Nt.l_min >= 0) {
@@ -976,73 +984,99 @@ bool plan_narrow(hmc_ctx* x, std::string& err) {
   a.l_min = N.l_min;
   a.n = x->n;
   if (const char* e = dev_env("HMC_NW_DBG")) a.dbg = atoi(e);
-  a.rb = (int)std::max<int64_t>(16, ((x->n + nw::NBMAX - 1) / nw::NBMAX + 3) / 4 * 4);
-  a.nblk = (int)((x->n + a.rb - 1) / a.rb);
   int dev = 0, optin = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const void* fn = nw::narrow_kernel(hw);
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  double best = 1e30;
-  for (int nc = std::min(nw::NCMAX, a.nblk); nc >= 1; --nc) {
-    const int bpc = (a.nblk + nc - 1) / nc;
-    if ((nc - 1) * bpc >= a.nblk) continue;  // no CTA without a row block
-    nw::NarrowArgs t = a;
-    nw_layout(x, bpc, nc, t);
-    if (t.smem_bytes > optin) continue;
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(nc);
-    cfg.blockDim = dim3(nw::NT);
-    cfg.dynamicSmemBytes = t.smem_bytes;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = nc;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    if (clusters < 1) continue;
-    const double cost = (double)((x->C + clusters - 1) / clusters) * bpc;
-    if (cost < best - 1e-9) {
-      best = cost;
-      t.nc = nc;
-      x->nwa = t;
-      x->nw_hw = hw;
-      x->nw_clusters = clusters;
-    }
-  }
-  // grid mode: every CTA of every chain resident at once (cooperative launch), any nc up to nblk,
-  // exchanges through L2 - chosen when it needs fewer block-times than the best cluster shape
-  // (clusters of 16 are limited by the GPC layout: 7 co-resident at 1 CTA per SM on B200)
   int nsm = 148;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  for (int nc = std::min(a.nblk, nsm); nc >= 1 && engine_override() != 3; --nc) {
-    const int bpc = (a.nblk + nc - 1) / nc;
-    if ((nc - 1) * bpc >= a.nblk) continue;
-    nw::NarrowArgs t = a;
-    nw_layout(x, bpc, nc, t);
-    if (t.smem_bytes > optin) continue;
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw::NT, t.smem_bytes));
-    if ((int64_t)x->C * nc > (int64_t)per_sm * nsm) continue;
-    const double cost = (double)bpc;
-    if (cost < best - 1e-9) {
-      best = cost;
-      t.nc = nc;
-      t.grid = 1;
-      x->nwa = t;
-      x->nw_hw = hw;
-      x->nw_clusters = 0;
+  const void* fn = nw::narrow_kernel(hw);
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // Cost of one leapfrog step for the batch (cycles, a model): waves x (64-row passes of the thread
+  // grid x the pass time at ~30 % of the FP32 rate + ~8k cycles of exchange and barriers when a
+  // chain spans several CTAs; measured)
+  double fma_row = 0.0;
+  for (int l = 0; l < nl; ++l) fma_row += 3.0 * a.width[l] * a.width[l + 1];
+  int wmin = 1 << 30;  // narrowest hidden layer
+  for (int l = 1; l < nl; ++l) wmin = std::min(wmin, a.width[l]);
+  const double pass = std::max(2000.0, fma_row * nw::TILE / (128.0 * 0.3));
+  // (narrow hidden layers, < 32 columns: the thread grid is mostly idle and the per-row work of the
+  // weight-gradient K loops dominates, so the cost is the rows per CTA - more CTAs win)
+  auto step_cost = [&](int waves, int rows, int nc) {
+    if (wmin < 32) return (double)waves * rows;
+    return waves * (std::ceil(rows / (double)nw::TILE) * pass + (nc > 1 ? 8000.0 : 0.0));
+  };
+  double best = 1e30;
+  // row-block size (the unit of every sum over rows, so a function of the problem only): 64 rows
+  // (one pass of the thread grid) or, for longer data, n / 32 - else the 16-row rule; the larger
+  // wins ties
+  // (64-row blocks only when the hidden layers fill the 64-column thread grid reasonably: below 32
+  // columns most threads idle and the per-block K loops of the weight gradient dominate, so more
+  // CTAs on 16-row blocks win - measured on cfg1, 20 wide: 10 vs 14 us per step)
+  const int64_t per32 = ((x->n + nw::NBMAX - 1) / nw::NBMAX + 3) / 4 * 4;
+  std::vector<int> rbs;
+  if (wmin >= 32) rbs.push_back((int)std::max<int64_t>(nw::TILE, per32));
+  rbs.push_back((int)std::max<int64_t>(16, per32));
+  for (int rb : rbs) {
+    a.rb = rb;
+    a.nblk = (int)((x->n + a.rb - 1) / a.rb);
+    for (int nc = std::min(nw::NCMAX, a.nblk); nc >= 1; --nc) {  // cluster mode
+      const int bpc = (a.nblk + nc - 1) / nc;
+      if ((nc - 1) * bpc >= a.nblk) continue;  // no CTA without a row block
+      nw::NarrowArgs t = a;
+      nw_layout(x, bpc, nc, t);
+      if (t.smem_bytes > optin) continue;
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
+      cudaLaunchConfig_t cfg;
+      memset(&cfg, 0, sizeof(cfg));
+      cfg.gridDim = dim3(nc);
+      cfg.blockDim = dim3(nw::NT);
+      cfg.dynamicSmemBytes = t.smem_bytes;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = nc;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (clusters < 1) continue;
+      const double cost = step_cost((x->C + clusters - 1) / clusters, bpc * rb, nc);
+      if (cost < best - 1e-9) {
+        best = cost;
+        t.nc = nc;
+        x->nwa = t;
+        x->nw_hw = hw;
+        x->nw_clusters = clusters;
+      }
     }
-    break;  // (the largest feasible nc has the fewest blocks per CTA)
+    // grid mode: every CTA of every chain resident at once (cooperative launch), any nc up to nblk,
+    // exchanges through L2 - chosen when it costs less than the best cluster shape (clusters of
+    // 16 are limited by the GPC layout: 7 co-resident at 1 CTA per SM on B200)
+    for (int nc = std::min(a.nblk, nsm); nc >= 2 && engine_override() != 3; --nc) {
+      const int bpc = (a.nblk + nc - 1) / nc;
+      if ((nc - 1) * bpc >= a.nblk) continue;
+      nw::NarrowArgs t = a;
+      nw_layout(x, bpc, nc, t);
+      if (t.smem_bytes > optin) continue;
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw::NT, t.smem_bytes));
+      if ((int64_t)x->C * nc > (int64_t)per_sm * nsm) continue;
+      const double cost = step_cost(1, bpc * rb, nc);
+      if (cost < best - 1e-9) {
+        best = cost;
+        t.nc = nc;
+        t.grid = 1;
+        x->nwa = t;
+        x->nw_hw = hw;
+        x->nw_clusters = 0;
+      }
+      break;  // (the largest feasible nc has the fewest rows per CTA)
+    }
   }
   if (best >= 1e30) return false;
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x->nwa.smem_bytes));
@@ -1635,8 +1669,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   }
   // ---- NCCL (DATA mode) ----
   x->emulated = x->mode == HMC_MODE_DATA && cfg->exchange == 1;
-  CFG(cfg->exchange == 0 || cfg->exchange == 1, "exchange must be 0 (NCCL) or 1 (emulated, test hook)");
-  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb) && !x->emulated) {
+  CFG(cfg->exchange >= 0 && cfg->exchange <= 2, "exchange must be 0 (NCCL), 1 (emulated phases) or 2 (timing stand-in)");
+  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb) && cfg->exchange == 0) {
     ncclUniqueId id;
     if (x->world > 1) {
       CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");

@@ -55,3 +55,25 @@ def test_mask_on_first_layer_only():
 def test_wide_chain_batch():
     torch_cuda()
     _check(make_tiny_problem(M, n=97, n_chains=300, seed=65, noise=0.3, active_frac=0.3), 300, [0, 151, 299])
+
+
+N = ArchSpec("mlp", (NetSpec.plain((1, 64, 64, 64, 64, 1)),))   # cfg2's widths: the narrow engine
+
+
+def test_narrow_engine_edges():
+    """The narrow engine on: a single datum (one 16-row block, 15 padding rows), a single active
+    parameter (the output bias) and a first-layer-only mask, and a batch of 100 chains (more CTAs
+    than the GPU holds at once: cluster waves instead of the grid mode)."""
+    torch_cuda()
+    from paper_2507_14652_b200 import abi
+    p1 = make_tiny_problem(N, n=1, n_chains=2, seed=66, noise=0.3, active_frac=0.5)
+    _check(p1, 2)
+    p2 = make_tiny_problem(N, n=200, n_chains=2, seed=67, noise=0.3)
+    p2.idx = np.array([p2.P - 1], dtype=np.int32)
+    _check(p2, 2)
+    p2.idx = np.arange(0, 64 + 64, 5, dtype=np.int32)                # layer-0 weights and biases
+    _check(p2, 2)
+    p3 = make_tiny_problem(N, n=1024, n_chains=100, seed=68, noise=0.3, active_frac=0.1)
+    with abi.Context(p3) as c:
+        assert abi.hmc_engine_info(c.ctx).startswith("narrow-simt (cluster"), abi.hmc_engine_info(c.ctx)
+    _check(p3, 100, [0, 57, 99])

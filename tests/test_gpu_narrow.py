@@ -193,9 +193,8 @@ def test_narrow_resume_batch_invariance_and_L0():
 
 def test_narrow_grid_and_cluster_modes_bitwise_equal():
     """cfg2's 8 chains do not fit as co-resident 16-CTA clusters (7 per GPU), so the batch runs the
-    grid mode (cooperative launch, 16 CTAs x 2 row blocks, exchanges through L2); a single chain
-    runs 32 CTAs x 1 block, and - forced with hmc_debug_set_engine(3) - one cluster (distributed
-    shared memory).  Every sum over data rows is fixed by the row blocks, so chain 3's gradient,
+    grid mode (cooperative launch, exchanges through L2); a single chain runs the planner's own
+    choice and - forced with hmc_debug_set_engine(3) - one cluster (distributed shared memory).  Every sum over data rows is fixed by the row blocks, so chain 3's gradient,
     trajectory and decision are bitwise the same in all three."""
     torch = torch_cuda()
     from paper_2507_14652_b200 import abi
@@ -211,7 +210,8 @@ def test_narrow_grid_and_cluster_modes_bitwise_equal():
         abi.hmc_debug_set_engine(forced)
         try:
             with abi.Context(one) as c:
-                assert ("cluster" if forced else "grid 32") in _engine(c), _engine(c)
+                if forced:
+                    assert "cluster" in _engine(c), _engine(c)
                 lp1, g1 = gpu_grad(c, th[3:4])
                 T1, LP1, G1, a1, d1 = _traj(c, th[3:4], lp1, g1, prob.eps, prob.L, 5)
         finally:
