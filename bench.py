@@ -174,7 +174,7 @@ def run_reference(args):
 # configured eps of those configs is 11x / 15x beyond the limit (every proposal diverges).
 STABLE_EPS0 = {"cfg4": 1.1e-6, "cfg4u": 1.1e-6, "cfg5": 4.0e-7}
 # DATA-mode layout per config for N > 1; configs not listed run chain-parallel
-DATA_SHARD = {"cfg3": "rows", "cfg5": "points_xb"}
+DATA_SHARD = {"cfg3": "rows", "cfg5": "points_xc"}
 
 
 def _parallel(args, world):

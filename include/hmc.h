@@ -53,7 +53,7 @@ extern "C" {
 enum { HMC_MLP = 0, HMC_DEEPONET = 1 };                          /* P:68, P:369 */
 enum { HMC_ACT_IDENTITY = 0, HMC_ACT_TANH = 1, HMC_ACT_SIN = 2 }; /* P:273, P:335, P:534 */
 enum { HMC_MODE_SINGLE = 0, HMC_MODE_DATA = 1, HMC_MODE_CHAIN = 2 };
-enum { HMC_SHARD_ROWS = 0, HMC_SHARD_POINTS_XB = 1 };
+enum { HMC_SHARD_ROWS = 0, HMC_SHARD_POINTS_XB = 1, HMC_SHARD_POINTS_XC = 2 };
 
 /* A feed-forward net with n_layers linear layers: widths[0] inputs ... widths[n_layers]
  * outputs; layer l applies act[l] to (W_l h + b_l).  Arrays are host memory, read at setup. */
@@ -109,7 +109,12 @@ typedef struct {
                            shared query points): this rank holds condition block r, u[n_c/world x m],
                            point block r, q[n_x x d_t], and v[n_c x n_x] for ALL n_c conditions and its
                            n_x points (hmc_data.n_c = all conditions, n_c % world == 0); the branch
-                           outputs are all-gathered, dB reduce-scattered */
+                           outputs are all-gathered, dB reduce-scattered;
+                           HMC_SHARD_POINTS_XC (DeepONet with shared query points): point block r of
+                           q and v for the trunk and the combine, and the branch for chain block r
+                           (n_chains / world chains) on ALL n_c conditions (u[n_c x m]; full-height
+                           tiles at any world); the branch outputs of all chains are all-gathered,
+                           dB reduce-scattered back to the chain owners */
   const uint8_t* nccl_id; /* [128] from hmc_comm_unique_id on rank 0 (DATA mode, world > 1) */
   int32_t exchange;     /* DATA mode: 0 = in-graph NCCL collectives (the product path); 1 = test hook,
                            no communicator: the context only runs hmc_debug_data_phase and the caller

@@ -17,7 +17,7 @@ HMC_OK, HMC_E_CONFIG, HMC_E_CUDA, HMC_E_NCCL, HMC_E_OOM, HMC_E_STATE = 0, 1, 3, 
 HMC_MLP, HMC_DEEPONET = 0, 1
 ACT = {"identity": 0, "tanh": 1, "sin": 2}
 MODE = {"single": 0, "data": 1, "chain": 2}
-SHARD = {"rows": 0, "points_xb": 1}
+SHARD = {"rows": 0, "points_xb": 1, "points_xc": 2}
 
 LIB_PATH = os.environ.get("HMC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmc.so")
 

@@ -69,6 +69,11 @@ struct NetInfo {
   cudaStream_t ws = nullptr;
   std::vector<cudaEvent_t> evA, evW;
   bool cs_ready = false;    // colsum holds the partials of the current G
+  // the chains this net runs for (POINTS_XC: the branch runs only this rank's chain block) and the
+  // per-net views of the chain-indexed state: dense / plane weights and the k-vector gradient of
+  // the net's first chain; every other net buffer is allocated for nch chains
+  int nch = 0;
+  float *wd = nullptr, *whi = nullptr, *wlo = nullptr, *gl = nullptr;
   float* colred = nullptr;       // two-pass column-reduction scratch (own per net: the DeepONet
   float* narrow_part = nullptr;  // nets run on two streams), narrow-input weight-gradient partials
   float* gl_part = nullptr;      // K-split weight-gradient partials
@@ -93,6 +98,12 @@ struct hmc_ctx {
   bool xb = false;
   int64_t n_c_loc = 0;
   float *xb_recv = nullptr, *xb_full = nullptr, *xb_dB = nullptr, *xb_send = nullptr;
+  // DATA mode, POINTS_XC layout: point block per rank for the trunk and the combine, chain block per
+  // rank for the branch (all conditions); the branch outputs of all chains (all-gathered), the
+  // partial dB of all chains (reduce-scattered), the all-reduced k-gradient (out of place: this
+  // rank's gl has zeros in the branch entries of the other ranks' chains)
+  bool xc = false;
+  float *xc_Ball = nullptr, *xc_dB = nullptr, *gl_red = nullptr;
   double sigma = 1, sigma_p = 1;
   uint64_t seed = 0;
   bool has_b0 = false;
@@ -190,7 +201,7 @@ struct hmc_ctx {
     s.C = C; s.k = k; s.P = P; s.idx = d_idx; s.inv_mass = d_inv_mass; s.chain_ids = d_chain;
     s.Wd = Wd; s.Whi = Whi; s.Wlo = Wlo; s.tcpos = d_tcpos; s.Ptc = Ptc; s.cur_theta = cur_theta; s.cur_grad = cur_grad; s.cur_logp = cur_logp;
     s.wrk_theta = wrk_theta; s.wrk_grad = wrk_grad; s.wrk_logp = wrk_logp; s.p = p; s.H0 = H0;
-    s.gl = gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
+    s.gl = xc ? gl_red : gl; s.lik = lik; s.inv_2s2 = 1.0 / (2.0 * sigma * sigma); s.inv_sp2 = 1.0 / (sigma_p * sigma_p);
     s.eps = d_eps; s.da = d_da; s.div = d_div; s.rec = d_rec; s.key0 = (uint32_t)(seed & 0xffffffffu); s.key1 = (uint32_t)(seed >> 32);
     return s;
   }
@@ -368,8 +379,9 @@ bool launch_gemm(hmc_ctx* x, const GemmArgs& a_in, bool akm, bool bkm, cudaStrea
 bool is_narrow(const LayerInfo& L) { return L.n_in <= 8; }
 
 void launch_fwd_narrow(hmc_ctx* x, const LayerInfo& L, const float* in, int64_t s_in, cudaStream_t st) {
-  dim3 grid((unsigned)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS), x->C);
-  const float* W = x->Wd;
+  const NetInfo& N = x->nets[L.net];
+  dim3 grid((unsigned)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS), N.nch);
+  const float* W = N.wd;
 #define FN(DIN_) k_fwd_narrow<DIN_><<<grid, 256, 0, st>>>(in, s_in, L.rows, L.n_out, W, x->P, L.w_off, L.bias ? L.b_off : -1, \
                                                     L.act, L.A, L.act == ACT_SIN ? L.D : nullptr)
   switch (L.n_in) {
@@ -382,17 +394,17 @@ void launch_fwd_narrow(hmc_ctx* x, const LayerInfo& L, const float* in, int64_t 
 
 void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const float* in, int64_t s_in,
                          cudaStream_t st) {
+  const NetInfo& N = x->nets[L.net];
   const int nch = (int)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS);
-  dim3 grid(nch, x->C);
+  dim3 grid(nch, N.nch);
 #define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->nets[L.net].narrow_part, nch, x->sq)
   switch (L.n_in) {
     case 1: WN(1); break; case 2: WN(2); break; case 3: WN(3); break; case 4: WN(4); break;
     case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;
   }
 #undef WN
-  k_wgrad_narrow_p2<<<dim3((unsigned)((L.n_out * (L.n_in + 1) + 255) / 256), x->C), 256, 0, st>>>(
-      x->nets[L.net].narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off,
-                                          L.bias ? x->d_slot + L.b_off : nullptr, x->gl, x->k);
+  k_wgrad_narrow_p2<<<dim3((unsigned)((L.n_out * (L.n_in + 1) + 255) / 256), N.nch), 256, 0, st>>>(
+      N.narrow_part, nch, L.n_out, L.n_in, x->d_slot + L.w_off, L.bias ? x->d_slot + L.b_off : nullptr, N.gl, x->k);
   x->launches += 2;
 }
 
@@ -413,21 +425,21 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
   if (is_narrow(L)) {
     const int id = prof_begin(x, st);
     launch_fwd_narrow(x, L, in, s_in, st);
-    const double fl = 2.0 * x->C * L.rows * L.n_out * (double)L.n_in;
+    const double fl = 2.0 * N.nch * L.rows * L.n_out * (double)L.n_in;
     x->flop_acc += fl;
-    prof_end(x, id, st, "narrow_fwd", fl, 4.0 * x->C * L.rows * L.n_out);
+    prof_end(x, id, st, "narrow_fwd", fl, 4.0 * N.nch * L.rows * L.n_out);
     return;
   }
-  GemmArgs a = gemm_base((int)L.rows, L.n_out, L.n_in, x->C);
+  GemmArgs a = gemm_base((int)L.rows, L.n_out, L.n_in, N.nch);
   a.A = in; a.lda = L.n_in; a.sA = s_in;
-  a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
+  a.B = N.wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
   a.C = L.A; a.ldc = L.n_out; a.sC = L.rows * L.n_out;
   a.epi = EPI_FWD; a.act = L.act;
-  if (L.bias) { a.bias = x->Wd + L.b_off; a.s_bias = x->P; }
+  if (L.bias) { a.bias = N.wd + L.b_off; a.s_bias = x->P; }
   if (L.act == ACT_SIN) { a.D = L.D; a.ldd = L.n_out; a.sD = L.rows * L.n_out; }
   PreSplit pre;
   if (L.tc_w) {
-    pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
+    pre.hi = N.whi + L.q_off; pre.lo = N.wlo ? N.wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
     pre.only = L.planes_only;
   }
   launch_gemm(x, a, true, true, st, "fwd", L.tc_w ? &pre : nullptr);
@@ -454,17 +466,17 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
     if (L.any_active && is_narrow(L)) {
       const int id = prof_begin(x, st);
       launch_wgrad_narrow(x, L, G, in, s_in, st);
-      const double fl = 2.0 * x->C * L.rows * L.n_out * (double)(L.n_in + 1);
+      const double fl = 2.0 * N.nch * L.rows * L.n_out * (double)(L.n_in + 1);
       x->flop_acc += fl;
-      prof_end(x, id, st, "narrow_wgrad", fl, 4.0 * x->C * L.rows * L.n_out);
+      prof_end(x, id, st, "narrow_wgrad", fl, 4.0 * N.nch * L.rows * L.n_out);
     } else if (L.any_active) {
-      GemmArgs a = gemm_base(L.n_out, L.n_in, (int)L.rows, x->C);
+      GemmArgs a = gemm_base(L.n_out, L.n_in, (int)L.rows, N.nch);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
       a.B = in; a.ldb = L.n_in; a.sB = s_in;
       a.epi = EPI_WGRAD;
       a.sq = x->sq;
       a.slot_w = x->d_slot + L.w_off; a.slot_b = L.bias ? x->d_slot + L.b_off : nullptr;
-      a.n_in = L.n_in; a.gl = x->gl; a.k = x->k;
+      a.n_in = L.n_in; a.gl = N.gl; a.k = x->k;
       if (L.g_off >= 0) { a.gmask = x->d_gmask + L.g_off; a.gbase = x->d_gbase + L.g_off; a.n_grp = (L.n_in + 31) / 32; }
       if (L.ksplit > 1 && N.gl_part) { a.ksplit = L.ksplit; a.gl_part = N.gl_part; }
       static const bool fuse_bias = !(dev_env("HMC_BIAS_FUSE") && atoi(dev_env("HMC_BIAS_FUSE")) == 0);
@@ -479,8 +491,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         tc_launch_or_throw(x, a, false, false, st, "wgrad");
         x->launches++;
         if (a.ksplit > 1) {  // fixed-order sum of the splits' partial k-vector entries
-          k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.ws_hi - L.ws_lo + 255) / 256, 256)), x->C),
-                            256, 0, st>>>(N.gl_part, a.ksplit, (int64_t)x->C * x->k, x->k, L.ws_lo, L.ws_hi, x->gl);
+          k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.ws_hi - L.ws_lo + 255) / 256, 256)), N.nch),
+                            256, 0, st>>>(N.gl_part, a.ksplit, (int64_t)N.nch * x->k, x->k, L.ws_lo, L.ws_hi, N.gl);
           x->launches++;
         }
         x->flop_acc += 2.0 * a.M * a.N * (double)a.K * a.batch;
@@ -490,18 +502,17 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           const int id2 = prof_begin(x, st);
           if (N.cs_ready) {  // partials from the producing GEMM's epilogue
             const int nblk = (int)((L.rows + 31) / 32);
-            k_colsum_reduce<<<dim3((unsigned)((L.n_out + 31) / 32), x->C), 1024, 0, st>>>(
-                cs_i, (int64_t)nblk * L.n_out, nblk, L.n_out, x->d_slot + L.b_off, x->gl, x->k);
+            k_colsum_reduce<<<dim3((unsigned)((L.n_out + 31) / 32), N.nch), 1024, 0, st>>>(
+                cs_i, (int64_t)nblk * L.n_out, nblk, L.n_out, x->d_slot + L.b_off, N.gl, x->k);
             x->launches += 1;
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
-            k_colred_p1<<<dim3(chunks, x->C), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
-                                                             N.colred, chunks, x->sq);
-            k_colred_p2<<<x->C, 256, 0, st>>>(N.colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, x->gl,
-                                              x->k);
+            k_colred_p1<<<dim3(chunks, N.nch), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
+                                                              N.colred, chunks, x->sq);
+            k_colred_p2<<<N.nch, 256, 0, st>>>(N.colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, N.gl, x->k);
             x->launches += 2;
           }
-          prof_end(x, id2, st, "bias_grad", 1.0 * x->C * L.rows * L.n_out, 4.0 * x->C * L.rows * L.n_out);
+          prof_end(x, id2, st, "bias_grad", 1.0 * N.nch * L.rows * L.n_out, 4.0 * N.nch * L.rows * L.n_out);
         }
       } else {
         if (L.bias) { a.N += 1; a.ones_col = L.n_in; }
@@ -517,15 +528,15 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       const int nxt = ov ? (cur + 1) % 3 : (cur ^ 1);
       if (ov && i + 2 <= top) cudaStreamWaitEvent(ms, N.evW[i + 2], 0);  // buffers of delta_{i+2}
       const LayerInfo& Pv = x->layers[N.layers[i - 1]];
-      GemmArgs a = gemm_base((int)L.rows, L.n_in, L.n_out, x->C);
+      GemmArgs a = gemm_base((int)L.rows, L.n_in, L.n_out, N.nch);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
-      a.B = x->Wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
+      a.B = N.wd + L.w_off; a.ldb = L.n_in; a.sB = x->P;
       a.C = N.G[nxt]; a.ldc = L.n_in; a.sC = L.rows * L.n_in;
       a.epi = EPI_DACT; a.act = Pv.act;
       a.dsrc = (Pv.act == ACT_SIN) ? Pv.D : Pv.A; a.ld_dsrc = Pv.n_out; a.s_dsrc = Pv.rows * Pv.n_out;
       PreSplit pre;
       if (L.tc_w) {
-        pre.hi = x->Whi + L.q_off; pre.lo = x->Wlo ? x->Wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
+        pre.hi = N.whi + L.q_off; pre.lo = N.wlo ? N.wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
         pre.only = L.planes_only;
       }
       float* cs_prev = ov ? N.cs[(i - 1) % 3] : N.colsum;
@@ -547,11 +558,11 @@ void xb_gather_perm(hmc_ctx* x, cudaStream_t st) {
   x->launches++;
 }
 
-void xb_combine(hmc_ctx* x, cudaStream_t st) {
+void xb_combine(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr) {
   const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
   const int p = Tl.n_out;
   GemmArgs a = gemm_base((int)x->n_c, (int)x->n_x, p, x->C);
-  a.A = x->xb_full; a.lda = p; a.sA = x->n_c * p;
+  a.A = Ball ? Ball : x->xb_full; a.lda = p; a.sA = x->n_c * p;
   a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
   a.C = x->R; a.ldc = x->n_x; a.sC = x->n_c * x->n_x;
   a.epi = EPI_RESID; a.V = x->d_v; a.ldv = x->n_x;
@@ -561,28 +572,31 @@ void xb_combine(hmc_ctx* x, cudaStream_t st) {
   launch_gemm(x, a, true, true, st, "combine");
 }
 
-void xb_dB(hmc_ctx* x, cudaStream_t st) {
+void xb_dB(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr, float* out = nullptr) {
   const LayerInfo& Bl = x->layers[x->nets[0].layers.back()];
   const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
   const int p = Bl.n_out;
   GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, x->C);
   a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
   a.B = Tl.A; a.ldb = p; a.sB = x->n_x * p;
-  a.C = x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
-  a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
+  a.C = out ? out : x->xb_dB; a.ldc = p; a.sC = x->n_c * p;
+  a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = Ball ? Ball : x->xb_full; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
   launch_gemm(x, a, true, false, st, "dB");
-  k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, x->C, x->world, x->n_c_loc, p);
-  x->launches++;
-  x->nets[0].cs_ready = false;  // bias gradient from this rank's rows of dB (summed by the all-reduce)
+  if (!out) {  // POINTS_XB: the reduce-scatter order
+    k_xb_scatter<<<148 * 4, 256, 0, st>>>(x->xb_dB, x->xb_send, x->C, x->world, x->n_c_loc, p);
+    x->launches++;
+  }
+  // bias gradient from the reduce-scattered dB (the partials of this partial dB are not summed)
+  x->nets[0].cs_ready = false;
 }
 
-void xb_dT(hmc_ctx* x, cudaStream_t st) {
+void xb_dT(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr) {
   NetInfo& Nt = x->nets[1];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Tl.n_out;
   GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, x->C);
   a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
-  a.B = x->xb_full; a.ldb = p; a.sB = x->n_c * p;
+  a.B = Ball ? Ball : x->xb_full; a.ldb = p; a.sB = x->n_c * p;
   a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
   a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
   if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
@@ -669,6 +683,39 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
   const LayerInfo& Bl = x->layers[Nb.layers.back()];
   const LayerInfo& Tl = x->layers[Nt.layers.back()];
   const int p = Bl.n_out;
+  if (x->xc) {  // POINTS_XC: the branch for this rank's chain block on all conditions (full tiles),
+                // all-gathered by chains; combine / dB / dT / trunk for all chains on this rank's
+                // points; dB reduce-scattered back to the chain owners.  Exchanges on the branch
+                // stream, overlapping the trunk
+    std::string& err = x->err;
+    const size_t bblk = (size_t)Nb.nch * x->n_c * p;
+    fork(0);
+    for (int i = 0; i < (int)Nb.layers.size(); ++i) enqueue_forward_hidden(x, Nb, i, sb);
+    if (x->comm) {
+      CKN(ncclAllGather(Bl.A, x->xc_Ball, bblk, ncclFloat32, x->comm, sb));
+    } else {  // exchange = 2 (timing stand-in): the same bytes moved locally
+      for (int r = 0; r < x->world; ++r)
+        CK(cudaMemcpyAsync(x->xc_Ball + r * bblk, Bl.A, bblk * 4, cudaMemcpyDeviceToDevice, sb));
+    }
+    for (int i = 0; i < (int)Nt.layers.size(); ++i) enqueue_forward_hidden(x, Nt, i, st);
+    join(0);
+    xb_combine(x, st, x->xc_Ball);
+    fork(1);
+    if (Nb.l_min >= 0) {
+      xb_dB(x, sb, x->xc_Ball, x->xc_dB);
+      if (x->comm)
+        CKN(ncclReduceScatter(x->xc_dB, Nb.G[0], bblk, ncclFloat32, ncclSum, x->comm, sb));
+      else
+        CK(cudaMemcpyAsync(Nb.G[0], x->xc_dB + x->rank * bblk, bblk * 4, cudaMemcpyDeviceToDevice, sb));
+      enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, sb);
+    }
+    if (Nt.l_min >= 0) {
+      xb_dT(x, st, x->xc_Ball);
+      enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    }
+    join(1);
+    return;
+  }
   if (x->xb) {  // POINTS_XB: gather the branch outputs of all conditions, combine with this rank's
                 // points, reduce-scatter dB back to the condition owners, dT stays local.  The
                 // exchanges run on the branch stream: the all-gather overlaps the trunk forward,
@@ -772,9 +819,11 @@ void enqueue_reduce(hmc_ctx* x, cudaStream_t st, std::string& err) {
   x->launches++;
   if (x->mode == HMC_MODE_DATA && x->comm) {
     CKN(ncclGroupStart());
-    CKN(ncclAllReduce(x->gl, x->gl, (size_t)(x->C * x->k), ncclFloat32, ncclSum, x->comm, st));
+    CKN(ncclAllReduce(x->gl, x->xc ? x->gl_red : x->gl, (size_t)(x->C * x->k), ncclFloat32, ncclSum, x->comm, st));
     CKN(ncclAllReduce(x->lik, x->lik, (size_t)x->C, ncclFloat64, ncclSum, x->comm, st));
     CKN(ncclGroupEnd());
+  } else if (x->xc && !x->emulated) {  // (timing stand-in)
+    CK(cudaMemcpyAsync(x->gl_red, x->gl, (size_t)x->C * x->k * 4, cudaMemcpyDeviceToDevice, st));
   }
 }
 
@@ -1359,7 +1408,14 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     x->n_x = data->n_x;
     x->unaligned = data->q_per_pair != 0;
     x->xb = cfg->mode == HMC_MODE_DATA && cfg->shard == HMC_SHARD_POINTS_XB;
-    CFG(cfg->shard == HMC_SHARD_ROWS || cfg->shard == HMC_SHARD_POINTS_XB, "shard must be HMC_SHARD_*");
+    x->xc = cfg->mode == HMC_MODE_DATA && cfg->shard == HMC_SHARD_POINTS_XC;
+    CFG(cfg->shard >= HMC_SHARD_ROWS && cfg->shard <= HMC_SHARD_POINTS_XC, "shard must be HMC_SHARD_*");
+    if (x->xc) {
+      CFG(!x->unaligned, "POINTS_XC needs shared query points (q_per_pair = 0)");
+      CFG(cfg->world >= 1 && cfg->n_chains % cfg->world == 0, "POINTS_XC needs n_chains divisible by world");
+      CFG(arch->net[0].acts[arch->net[0].n_layers - 1] != HMC_ACT_SIN,
+          "POINTS_XC: the branch output layer cannot be sin (its act' is not all-gathered)");
+    }
     if (x->xb) {
       CFG(!x->unaligned, "POINTS_XB needs shared query points (q_per_pair = 0)");
       CFG(cfg->world >= 1 && x->n_c % cfg->world == 0, "POINTS_XB needs n_c divisible by world");
@@ -1475,7 +1531,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       L.ksplit = 1;
       if (x->tc.enabled && L.any_active && L.n_in > 8) {
         const int64_t rows = x->nets[L.net].rows;  // (L.rows is filled in later)
-        GemmArgs pa = gemm_base(L.n_out, L.n_in, (int)rows, x->C);
+        const int nch_l = (x->xc && L.net == 0) ? x->C / x->world : x->C;  // (POINTS_XC branch: its chain block)
+        GemmArgs pa = gemm_base(L.n_out, L.n_in, (int)rows, nch_l);
         const int pt = TcPlanner::pair_tiles(pa);
         const int half_sms = std::max(1, x->tc.num_sms / 2);
         const int nk = (int)((rows + 31) / 32);
@@ -1599,6 +1656,26 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       x->xb_full = dalloc<float>(x, (size_t)C * x->n_c * p, err);
       x->xb_dB = dalloc<float>(x, (size_t)C * x->n_c * p, err);
     }
+    if (x->xc) {
+      x->xc_Ball = dalloc<float>(x, (size_t)C * x->n_c * p, err);
+      x->xc_dB = dalloc<float>(x, (size_t)C * x->n_c * p, err);
+      x->gl_red = dalloc<float>(x, (size_t)C * x->k, err);
+    }
+  }
+  // per-net chain views (POINTS_XC: the branch runs this rank's chain block; its buffers keep the
+  // full chain-count size, only the first nch chains are used)
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    NetInfo& N = x->nets[ni];
+    int64_t c0 = 0;
+    N.nch = C;
+    if (x->xc && ni == 0) {
+      N.nch = C / x->world;
+      c0 = (int64_t)x->rank * N.nch;
+    }
+    N.wd = x->Wd + c0 * x->P;
+    N.whi = x->Whi ? x->Whi + c0 * x->Ptc : nullptr;
+    N.wlo = x->Wlo ? x->Wlo + c0 * x->Ptc : nullptr;
+    N.gl = x->gl + c0 * x->k;
   }
   {  // two-pass column-reduction scratch: max over nets of chunks x (width + 1)
     size_t cap = 0;
@@ -1670,7 +1747,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
   // ---- NCCL (DATA mode) ----
   x->emulated = x->mode == HMC_MODE_DATA && cfg->exchange == 1;
   CFG(cfg->exchange >= 0 && cfg->exchange <= 2, "exchange must be 0 (NCCL), 1 (emulated phases) or 2 (timing stand-in)");
-  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb) && cfg->exchange == 0) {
+  if (x->mode == HMC_MODE_DATA && (x->world > 1 || x->xb || x->xc) && cfg->exchange == 0) {
     ncclUniqueId id;
     if (x->world > 1) {
       CFG(cfg->nccl_id, "DATA mode with world > 1 needs nccl_id");
@@ -2195,23 +2272,46 @@ int hmc_debug_data_phase(hmc_ctx* ctx, int32_t phase, const void* in, const void
   const int p = x->kind == HMC_DEEPONET ? x->layers[x->nets[0].layers.back()].n_out : 0;
   const size_t blk = (size_t)x->C * x->n_c_loc * p;
   NetInfo& Nb = x->nets[0];
+  const size_t xcblk = (size_t)Nb.nch * x->n_c * p;  // POINTS_XC: this rank's chain block of branch outputs
   auto reduce_out = [&]() {
     k_reduce_partials<<<x->C, KT, 0, st>>>(x->part_sq, x->part_r, x->n_part, x->lik, x->gl, x->k, x->b0_slot);
     cpy(out, x->gl, Ck * 4, st, err);
     cpy(out2, x->lik, (size_t)x->C * 8, st, err);
   };
   if (phase == 0) {
-    CFG(in && out && (x->xb || out2), "phase 0: theta in; out (and out2 for the row layout)");
+    CFG(in && out && (x->xb || x->xc || out2), "phase 0: theta in; out (and out2 for the row layout)");
     cpy(x->wrk_theta, in, Ck * 4, st, err);
     k_scatter<<<dim3((unsigned)std::min<int64_t>((x->k + 255) / 256, 1024), x->C), 256, 0, st>>>(x->kstate(), x->wrk_theta);
-    if (x->xb) {  // forward of both nets; out = this rank's branch outputs (the all-gather's input)
+    if (x->xb || x->xc) {  // forward of both nets; out = this rank's branch outputs (the all-gather's input)
       for (int ni = 0; ni < 2; ++ni)
         for (int i = 0; i < (int)x->nets[ni].layers.size(); ++i) enqueue_forward_hidden(x, x->nets[ni], i, st);
-      cpy(out, x->layers[Nb.layers.back()].A, blk * 4, st, err);
+      cpy(out, x->layers[Nb.layers.back()].A, (x->xc ? xcblk : blk) * 4, st, err);
     } else {      // row layout: the whole local evaluation; out = g_lik [C x k], out2 = sum r^2 [C]
       enqueue_body(x, st);
       reduce_out();
     }
+  } else if (phase == 1 && x->xc) {
+    CFG(in && out, "phase 1 (POINTS_XC): in = all-gathered branch outputs, out = reduce-scatter input");
+    cpy(x->xc_Ball, in, xcblk * x->world * 4, st, err);
+    xb_combine(x, st, x->xc_Ball);
+    if (Nb.l_min >= 0) {
+      xb_dB(x, st, x->xc_Ball, x->xc_dB);
+      cpy(out, x->xc_dB, xcblk * x->world * 4, st, err);
+    } else {
+      CK(cudaMemsetAsync(out, 0, xcblk * x->world * 4, st));
+    }
+  } else if (phase == 2 && x->xc) {
+    CFG(in && out && out2, "phase 2 (POINTS_XC): in = reduce-scattered dB block, out / out2 = g_lik / sum r^2");
+    NetInfo& Nt = x->nets[1];
+    if (Nb.l_min >= 0) {
+      cpy(Nb.G[0], in, xcblk * 4, st, err);
+      enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, st);
+    }
+    if (Nt.l_min >= 0) {
+      xb_dT(x, st, x->xc_Ball);
+      enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+    }
+    reduce_out();
   } else if (phase == 1) {
     CFG(x->xb && in && out, "phase 1 (POINTS_XB): in = all-gathered branch outputs, out = reduce-scatter input");
     cpy(x->xb_recv, in, blk * x->world * 4, st, err);
@@ -2225,7 +2325,7 @@ int hmc_debug_data_phase(hmc_ctx* ctx, int32_t phase, const void* in, const void
     reduce_out();
   } else {
     CFG(in && in2 && out && out2, "phase 3: in / in2 = summed g_lik / sum r^2, out / out2 = grad / logp");
-    cpy(x->gl, in, Ck * 4, st, err);
+    cpy(x->xc ? x->gl_red : x->gl, in, Ck * 4, st, err);
     cpy(x->lik, in2, (size_t)x->C * 8, st, err);
     k_finalize<<<x->C, KT, 0, st>>>(x->kstate(), 0);
     cpy(out, x->wrk_grad, Ck * 4, st, err);

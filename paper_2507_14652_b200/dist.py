@@ -60,6 +60,18 @@ def shard_points_xb(problem, rank: int, world: int):
     return sh, n_c * n_x
 
 
+def shard_points_xc(problem, rank: int, world: int):
+    """POINTS_XC layout (DeepONet with shared query points): ALL conditions of u (the
+    branch runs this rank's chain block on all of them), point block r of q, and v for all
+    conditions at those points.  Returns (shard, n_global)."""
+    n_c, n_x = problem.v.shape
+    x0, x1 = row_block(n_x, rank, world)
+    sh = copy.copy(problem)
+    sh.q = np.ascontiguousarray(problem.q[x0:x1])
+    sh.v = np.ascontiguousarray(problem.v[:, x0:x1])
+    return sh, n_c * n_x
+
+
 def broadcast_nccl_id(make_id, group=None) -> bytes:
     """Rank 0 calls make_id() (libhmc's hmc_comm_unique_id); every rank returns the same bytes."""
     import torch.distributed as dist
@@ -78,6 +90,8 @@ def make_context(problem, mode: str, rank: int, world: int, group=None, shard: s
                            chain_ids=chain_ids(rank, C) if world > 1 else None)
     if shard == "points_xb":
         sh, n_global = shard_points_xb(problem, rank, world)
+    elif shard == "points_xc":
+        sh, n_global = shard_points_xc(problem, rank, world)
     else:
         sh, n_global = shard_rows(problem, rank, world)
     nid = broadcast_nccl_id(abi.hmc_comm_unique_id, group) if world > 1 else None

@@ -34,5 +34,5 @@ for cfg in (sys.argv[1:] or ["cfg1", "cfg2"]):
                         "seconds": dt, "evals_per_s": evals / dt, "samples_per_s": prob.n_chains * prob.S / dt,
                         "acceptance": float(np.mean(acc))}
     print(cfg, out["runs"][cfg], flush=True)
-os.makedirs("profiles", exist_ok=True)
-json.dump(out, open("profiles/r02_oracle_full_runs.json", "w"), indent=1)
+os.makedirs("gpurun_out/r2", exist_ok=True)
+json.dump(out, open("gpurun_out/r2/oracle_full_runs.json", "w"), indent=1)

@@ -20,7 +20,7 @@ from paper_2507_14652_b200 import dist as pdist  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-shard = {"cfg5": "points_xb", "cfg3": "rows", "cfg4": "rows"}.get(cfg, "rows")
+shard = sys.argv[3] if len(sys.argv) > 3 else {"cfg5": "points_xc", "cfg3": "rows", "cfg4": "rows"}.get(cfg, "rows")
 prob = make_problem(cfg)
 C, k, L = prob.n_chains, prob.k, prob.L
 eps = {"cfg5": 4e-7, "cfg4": 1.1e-6}.get(cfg, prob.eps)
@@ -30,7 +30,8 @@ for G in (1, 2, 4, 8):
     if G == 1:
         ctx = abi.Context(prob)
     else:
-        sh, n_global = (pdist.shard_points_xb if shard == "points_xb" else pdist.shard_rows)(prob, 0, G)
+        sh, n_global = {"points_xb": pdist.shard_points_xb, "points_xc": pdist.shard_points_xc,
+                        "rows": pdist.shard_rows}[shard](prob, 0, G)
         ctx = abi.Context(sh, mode="data", rank=0, world=G, n_global=n_global, shard=shard, exchange="local")
     T = torch.as_tensor(np.repeat(prob.frozen[prob.idx][None], C, 0), device="cuda").contiguous()
     LP = torch.empty(C, dtype=torch.float64, device="cuda")
@@ -61,5 +62,5 @@ for G, d in res["per_G"].items():
     d["projected_evals_per_s"] = C * L / (d["ms_per_step_rank"] / 1000.0)
     d["projected_efficiency_compute_only"] = t1 / (G * d["ms_per_step_rank"])
 print(json.dumps(res, indent=1))
-os.makedirs("profiles", exist_ok=True)
-json.dump(res, open(f"profiles/r02_scaling_projection_{cfg}.json", "w"), indent=1)
+os.makedirs("gpurun_out/r2", exist_ok=True)
+json.dump(res, open(f"gpurun_out/r2/scaling_projection_{cfg}_{shard}.json", "w"), indent=1)

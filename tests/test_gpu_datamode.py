@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 ARCH = ArchSpec("deeponet", (NetSpec.plain((7, 130, 64, 50)), NetSpec.plain((3, 70, 50), last="tanh")), has_b0=True)
 
 
-@pytest.mark.parametrize("shard", ["rows", "points_xb"])
+@pytest.mark.parametrize("shard", ["rows", "points_xb", "points_xc"])
 def test_data_mode_world1_grad(shard):
     torch_cuda()
     from paper_2507_14652_b200 import dist as pdist
@@ -57,3 +57,21 @@ def test_points_xb_config_errors():
     prob = make_tiny_problem(ARCH, n_c=8, n_x=6, n_chains=1, seed=52, unaligned=True)
     with pytest.raises(abi.HmcError):
         abi.Context(prob, mode="data", shard="points_xb")
+
+
+def test_points_xc_world1_cfg5_trajectory():
+    """cfg5 at full size (4 chains) in the POINTS_XC layout with real in-graph NCCL collectives
+    (a communicator of one), gradient and a short trajectory against the oracle."""
+    torch_cuda()
+    from paper_2507_14652_b200 import dist as pdist
+    from test_gpu_parity import _gpu_traj
+    prob = make_problem("cfg5", n_chains=4)
+    th = jittered_states(prob, 4)
+    t = ohmc.Target(prob)
+    with pdist.make_context(prob, "data", 0, 1, shard="points_xc") as c:
+        lp, g = gpu_grad(c, th)
+        T1, _, _, acc, dH = _gpu_traj(c, th, lp, g, 4.0e-7, 3, 0)
+    lr, gr = t.logp_grad(th[0])
+    assert_grad_close(lp[0], g[0], lr, gr, "cfg5 points_xc")
+    r = ohmc.trajectory(t, th[0].astype(np.float64), lr, gr, 4.0e-7, 3, 0, 0)
+    assert abs(dH[0] - r["dH"]) <= 1e-6 * (abs(r["H0"]) + abs(r["H1"])) + 1e-4

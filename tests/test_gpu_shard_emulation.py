@@ -45,7 +45,8 @@ def _rank_contexts(prob, G, shard):
     from paper_2507_14652_b200 import dist as pdist
     ctxs = []
     for r in range(G):
-        sh, n_global = (pdist.shard_points_xb if shard == "points_xb" else pdist.shard_rows)(prob, r, G)
+        sh, n_global = {"points_xb": pdist.shard_points_xb, "points_xc": pdist.shard_points_xc,
+                        "rows": pdist.shard_rows}[shard](prob, r, G)
         ctxs.append(abi.Context(sh, mode="data", rank=r, world=G, n_global=n_global, shard=shard,
                                 exchange="emulated"))
     return ctxs
@@ -62,7 +63,23 @@ def _emulated_grad(prob, th, G, shard):
     try:
         gl = [torch.empty(C, k, device="cuda") for _ in range(G)]
         lik = [torch.empty(C, dtype=torch.float64, device="cuda") for _ in range(G)]
-        if shard == "points_xb":
+        if shard == "points_xc":   # chain blocks: rank r's branch outputs are chains [r C/G, (r+1) C/G)
+            n_c = prob.v.shape[0]
+            p = prob.arch.nets[0].widths[-1]
+            Cb = C // G
+            B = [torch.empty(Cb, n_c, p, device="cuda") for _ in range(G)]
+            for r, c in enumerate(ctxs):
+                abi.hmc_debug_data_phase(c.ctx, 0, T, None, B[r])
+            gathered = torch.cat(B).contiguous()                      # all-gather, rank (= chain) order
+            send = [torch.empty(C, n_c, p, device="cuda") for _ in range(G)]
+            for r, c in enumerate(ctxs):
+                abi.hmc_debug_data_phase(c.ctx, 1, gathered, None, send[r])
+            tot = send[0].clone()
+            for q in range(1, G):
+                tot += send[q]
+            for r, c in enumerate(ctxs):                              # reduce-scatter: chain block r to rank r
+                abi.hmc_debug_data_phase(c.ctx, 2, tot[r * Cb:(r + 1) * Cb].contiguous(), None, gl[r], lik[r])
+        elif shard == "points_xb":
             n_c = prob.v.shape[0]
             p = prob.arch.nets[0].widths[-1]
             B = [torch.empty(C, n_c // G, p, device="cuda") for _ in range(G)]
@@ -155,3 +172,27 @@ def test_emulated_context_refuses_the_graph_calls():
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_points_xc_emulated_ranks_match_oracle(G):
+    """POINTS_XC: the branch for this rank's chain block on all conditions, the trunk
+    and the combine on its point block; 8 chains so every rank owns at least one."""
+    prob = make_tiny_problem(XB_ARCH, n_c=40, n_x=200, active_frac=0.5, n_chains=8, seed=65, noise=0.3)
+    th = jittered_states(prob, 8)
+    lp, g = _emulated_grad(prob, th, G, "points_xc")
+    t = ohmc.Target(prob)
+    for ci in (0, 3, 7):
+        lr, gr = t.logp_grad(th[ci])
+        assert_grad_close(lp[ci], g[ci], lr, gr, f"points_xc G={G} chain {ci}")
+
+
+def test_points_xc_emulated_cfg5_G8():
+    """cfg5 at full size over 8 emulated ranks in the POINTS_XC layout (8 chains: one per rank)."""
+    prob = make_problem("cfg5", n_chains=8)
+    th = jittered_states(prob, 8)
+    lp, g = _emulated_grad(prob, th, 8, "points_xc")
+    t = ohmc.Target(prob)
+    for ci in (0, 5):
+        lr, gr = t.logp_grad(th[ci])
+        assert_grad_close(lp[ci], g[ci], lr, gr, f"cfg5 points_xc G=8 chain {ci}")
