@@ -156,3 +156,72 @@ def test_points_xb_exchange_matches_full_batch():
         assert n_global == 12 * 9
         np.testing.assert_allclose(buf[:-1], g_ref, rtol=1e-11, atol=1e-11 * np.abs(g_ref).max())
         assert buf[-1] == pytest.approx(ll, rel=1e-12)
+
+
+def _xc_worker(rank, world, port, q):
+    """POINTS_XC algebra with the oracle's per-net passes, 2 chains over 2 ranks:
+    rank r runs the branch for chain r on ALL conditions and the trunk for both chains on its
+    points; B all-gathered by chain; residuals of both chains at its points; dB of both chains
+    reduce-scattered by chain; the branch backward of its chain, the trunk backward of both; the
+    all-reduce of [g_lik, sum r^2] per chain == the full-batch values."""
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import network as onet
+    arch, prob = _xb_case()
+    sh, n_global = pdist.shard_points_xc(prob, rank, world)
+    thetas = [prob.frozen.astype(np.float64) + 0.01 * (c + 1) for c in range(world)]   # chain c's parameters
+    _, b0, _ = onet.layer_table(arch)
+    s2 = prob.noise_sigma ** 2
+    Bown, tb = onet.net_forward(arch, thetas[rank], 0, sh.u.astype(np.float64))   # chain = rank, all conditions
+    parts = [torch.zeros_like(torch.as_tensor(Bown)) for _ in range(world)]
+    dist.all_gather(parts, torch.as_tensor(Bown))                                   # B of every chain
+    bufs = []
+    dB_parts = []
+    tapes_t = []
+    Es = []
+    for c in range(world):
+        T, tt = onet.net_forward(arch, thetas[c], 1, sh.q.astype(np.float64))
+        Ball = parts[c].numpy()
+        R = sh.v.astype(np.float64) - (Ball @ T.T + thetas[c][b0])
+        E = R / s2
+        Es.append((E, R, Ball, tt))
+        dB_parts.append(torch.as_tensor(E @ T))                  # chain c, all conditions, own points
+    dB_own = torch.zeros_like(dB_parts[0])
+    dist.reduce_scatter(dB_own, dB_parts)                         # chain block (= rank) gets its full dB
+    for c in range(world):
+        E, R, Ball, tt = Es[c]
+        g = np.zeros_like(thetas[c])
+        if c == rank:
+            onet.net_backward(arch, thetas[c], 0, tb, dB_own.numpy(), g)    # branch: own chain only
+        onet.net_backward(arch, thetas[c], 1, tt, E.T @ Ball, g)          # trunk: every chain, own points
+        g[b0] += E.sum()
+        bufs.append(np.concatenate([g, [-np.sum(R * R) / (2 * s2)]]))
+    buf = torch.tensor(np.stack(bufs), dtype=torch.float64)
+    dist.all_reduce(buf)
+    q.put((rank, buf.numpy(), n_global))
+    dist.destroy_process_group()
+
+
+def test_points_xc_exchange_matches_full_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import network as onet
+    arch, prob = _xb_case()
+    data = {"u": prob.u.astype(np.float64), "q": prob.q.astype(np.float64), "v": prob.v.astype(np.float64)}
+    for rank, buf, n_global in res:
+        assert n_global == 12 * 9
+        for c in range(2):
+            th = prob.frozen.astype(np.float64) + 0.01 * (c + 1)
+            ll, g_ref, _ = onet.loglik_grad(arch, th, data, prob.noise_sigma)
+            np.testing.assert_allclose(buf[c, :-1], g_ref, rtol=1e-11, atol=1e-11 * np.abs(g_ref).max())
+            assert buf[c, -1] == pytest.approx(ll, rel=1e-12)
