@@ -61,8 +61,8 @@ struct NarrowArgs {
   // co-resident clusters): the exchanges go through L2 instead of distributed shared memory and
   // the barriers are per-chain counters
   int grid;
-  float* xpart;               // [C][nc][nblk][ksp] block partials, by owner slice
   float* xtheta;              // [C][k] the new theta of the step
+  float* xpart;               // [C][nc][nblk][ksp] block partials, by owner slice
   double* xsq;                // [C][nblk] sum r^2 per block
   unsigned* xbar;             // [C] barrier counters (zeroed before every launch)
   int dbg;                    // dev experiments (HMC_NW_DBG, -DHMC_DEV only): bit 0 skip weight-gradient
@@ -325,6 +325,42 @@ __device__ __forceinline__ void wgrad_layer(const float* __restrict__ D, int ldd
   const int n_in = IC ? IC : nin_rt;
   const int ldd = LD ? LD : ldd_rt, lda = LA ? LA : lda_rt;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  if (!IC && n_in <= 4) {
+    // a narrow input (the first layer): dW[o][i] for i < n_in the way the bias is reduced below -
+    // thread (ty, tx) sums rows r = tx (mod 16) of columns 4 ty .. 4 ty + 3 times A[r][i], then a
+    // fixed xor-butterfly over the 16 lanes of its half-warp (the 4 x 4 register tiles would
+    // leave all but one thread in 16 idle)
+    for (int ob = 0; ob < n_out; ob += TILE) {
+      const int o0 = ob + 4 * ty;
+      for (int i = 0; i < n_in; ++i) {
+        int sl[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) sl[m] = o0 + m < n_out ? slot_w[(o0 + m) * n_in + i] : -1;
+        for (int b = 0; b < nb; ++b) {
+          float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (o0 < n_out)
+            for (int r = tx; r < rb; r += 16) {
+              const float4 d = *reinterpret_cast<const float4*>(D + (b * rb + r) * ldd + o0);
+              const float av = A[(b * rb + r) * lda + i];
+              s.x = fmaf(d.x, av, s.x); s.y = fmaf(d.y, av, s.y); s.z = fmaf(d.z, av, s.z); s.w = fmaf(d.w, av, s.w);
+            }
+#pragma unroll
+          for (int off = 8; off > 0; off >>= 1) {
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, off);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, off);
+            s.z += __shfl_xor_sync(0xffffffffu, s.z, off);
+            s.w += __shfl_xor_sync(0xffffffffu, s.w, off);
+          }
+          if (tx == 0) {
+            const float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (sl[m] >= 0) push.put(sl[m], b, sv[m]);
+          }
+        }
+      }
+    }
+  } else
 #pragma unroll
   for (int ob = 0; ob < (OC ? OC : 1 << 30); ob += TILE) {
     if (!OC && ob >= n_out) break;
@@ -546,42 +582,59 @@ __global__ void __launch_bounds__(NT, 1) k_narrow(KState s, NarrowArgs a, int ns
       const float b = sm[a.sb[out_l]];
       const int warp = tid >> 5, lane = tid & 31;
       const int kin = (n_in + 3) & ~3;  // (padding columns of A and w are zero)
-      for (int r = tid; r < rows; r += NT) {  // one thread per row, inputs in order
+      // four threads per row: float4 input chunks q, q + 4, ..., then a fixed xor-butterfly
+      for (int t = tid; t < 4 * ((rows + 63) / 64) * 64; t += NT) {
+        const int r = t >> 2, q = t & 3;
         float f = 0.f;
-        for (int i = 0; i < kin; i += 4) {
-          const float4 av = *reinterpret_cast<const float4*>(A + r * lda + i);
-          const float4 wv = *reinterpret_cast<const float4*>(w + i);
-          f = fmaf(av.x, wv.x, f);
-          f = fmaf(av.y, wv.y, f);
-          f = fmaf(av.z, wv.z, f);
-          f = fmaf(av.w, wv.w, f);
+        if (r < rows)
+          for (int i = 4 * q; i < kin; i += 16) {
+            const float4 av = *reinterpret_cast<const float4*>(A + r * lda + i);
+            const float4 wv = *reinterpret_cast<const float4*>(w + i);
+            f = fmaf(av.x, wv.x, f);
+            f = fmaf(av.y, wv.y, f);
+            f = fmaf(av.z, wv.z, f);
+            f = fmaf(av.w, wv.w, f);
+          }
+        f += __shfl_xor_sync(0xffffffffu, f, 1);
+        f += __shfl_xor_sync(0xffffffffu, f, 2);
+        if (q == 0 && r < rows) {
+          const float rr = row0 + r < a.n ? ys[r] - (f + b) : 0.f;
+          Rr[r] = rr;
+          R[r] = rr * a.inv_s2;
         }
-        const float rr = row0 + r < a.n ? ys[r] - (f + b) : 0.f;
-        Rr[r] = rr;
-        R[r] = rr * a.inv_s2;
       }
       __syncthreads();
-      if (mode != 1 && tid < my_blocks) {  // sum r^2 of block tid, rows in order (fp64)
-        double sq = 0.0;
-        for (int r = tid * a.rb; r < (tid + 1) * a.rb; ++r) sq += (double)Rr[r] * (double)Rr[r];
-        red[tid] = sq;
-        if (a.grid) __stcg(a.xsq + (int64_t)c * a.nblk + rank * a.bpc + tid, sq);
-      }
+      if (mode != 1)  // sum r^2 of each block (fp64): a warp per block, lanes over rows, butterfly
+        for (int blk = warp; blk < my_blocks; blk += NT / 32) {
+          double sq = 0.0;
+          for (int r = blk * a.rb + lane; r < (blk + 1) * a.rb; r += 32) sq += (double)Rr[r] * (double)Rr[r];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          if (lane == 0) {
+            red[blk] = sq;
+            if (a.grid) __stcg(a.xsq + (int64_t)c * a.nblk + rank * a.bpc + blk, sq);
+          }
+        }
       // output-layer weight / bias gradient of each block: dw[i] = sum_r R[r] A[r][i], db = sum_r R[r]
-      // (one thread per (block, input), rows in order)
+      // (four threads per (block, input): rows q, q + 4, ..., then a fixed xor-butterfly)
       const SlotRef slw = slot.off(a.w_off[out_l]);
-      for (int t = tid; t < (my_blocks > 0 ? my_blocks : 0) * (n_in + 1); t += NT) {
-        const int blk = t / (n_in + 1), i = t - blk * (n_in + 1);
-        if (i == n_in && a.b_off[out_l] < 0) continue;
-        const int sl = i < n_in ? slw[i] : slot[a.b_off[out_l]];
-        if (sl < 0) continue;
+      const int ntask = (my_blocks > 0 ? my_blocks : 0) * (n_in + 1);
+      for (int t = tid; t < 4 * ((ntask + 63) / 64) * 64; t += NT) {
+        const int task = t >> 2, q = t & 3;
+        const int blk = task / (n_in + 1), i = task - blk * (n_in + 1);
+        int sl = -1;
+        if (task < ntask && !(i == n_in && a.b_off[out_l] < 0)) sl = i < n_in ? slw[i] : slot[a.b_off[out_l]];
         float g = 0.f;
-        const int r0 = blk * a.rb;
-        if (i < n_in)
-          for (int r = r0; r < r0 + a.rb; ++r) g = fmaf(R[r], A[r * lda + i], g);
-        else
-          for (int r = r0; r < r0 + a.rb; ++r) g += R[r];
-        push.put(sl, blk, g);
+        if (sl >= 0) {
+          const int r0 = blk * a.rb;
+          if (i < n_in)
+            for (int r = r0 + q; r < r0 + a.rb; r += 4) g = fmaf(R[r], A[r * lda + i], g);
+          else
+            for (int r = r0 + q; r < r0 + a.rb; r += 4) g += R[r];
+        }
+        g += __shfl_xor_sync(0xffffffffu, g, 1);
+        g += __shfl_xor_sync(0xffffffffu, g, 2);
+        if (q == 0 && sl >= 0) push.put(sl, blk, g);
       }
       __syncthreads();
       // delta of the top hidden layer, in place: D[r][i] = R[r] w[i] act'(A[r][i])
