@@ -271,9 +271,11 @@ int hmc_debug_xb_permute(int32_t dir, int32_t C, int32_t G, int64_t n_loc, int32
 
 /* Test hook, process-wide, read by hmc_setup: mode 0 = automatic (the narrow-network cluster
  * engine for MLPs that qualify, else tcgen05 wherever it takes the shape and SIMT elsewhere);
- * 1 = every GEMM on the per-layer SIMT FP32 engine; 2 = the per-layer engines only (no narrow
- * engine); 3 = the narrow engine restricted to its cluster mode (no cooperative grid mode).
- * Returns HMC_E_CONFIG for any other mode.  Developer knobs of the tcgen05 engine (HMC_TC_* environment
+ * 1 = every GEMM on the per-layer SIMT FP32 engine; 2 = the per-layer dense engines only (no narrow
+ * engine, no masked weight gradient); 3 = the narrow engine restricted to its cluster mode (no cooperative grid mode);
+ * 4 = the per-layer engines with the masked weight gradient (sampled dense-dense kernel over the
+ * mask's entries) on every hidden layer it takes, whatever the planner's cost model
+ * would choose.  Returns HMC_E_CONFIG for any other mode.  Developer knobs of the tcgen05 engine (HMC_TC_* environment
  * variables: barrier profiles, timelines, A/B toggles) are compiled in only with -DHMC_DEV
  * (`make DEV=1`); the product library ignores the environment. */
 int hmc_debug_set_engine(int32_t mode);

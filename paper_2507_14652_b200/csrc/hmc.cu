@@ -16,6 +16,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <array>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -23,6 +25,7 @@
 #include "../../include/hmc.h"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "masked_wgrad.cuh"
 #include "narrow.cuh"
 #include "partition.cuh"
 #include "tc_gemm.cuh"
@@ -51,6 +54,12 @@ struct LayerInfo {
   int64_t g_off = -1;          // offset of this layer's [n_out x ceil(n_in/32)] group masks (d_gmask)
   int64_t ws_lo = 0, ws_hi = 0; // k-slot range of this layer's active weights
   int ksplit = 1;               // K split of its tensor-core weight-gradient GEMM
+  // masked weight gradient (masked_wgrad.cuh) instead of the dense GEMM: task list, row segments,
+  // task blocks, the k-slot range of the layer's active weights and bias
+  bool mwg = false;
+  int mw_seg = 1, mw_tb = 1;
+  MwTasks mw{};
+  int64_t mw_lo = 0, mw_hi = 0, mw_pairs = 0;
   float* A = nullptr;  // [C x rows x n_out] layer output (hidden layers)
   float* D = nullptr;  // [C x rows x n_out] cos(z) for sin layers
 };
@@ -77,6 +86,7 @@ struct NetInfo {
   float* colred = nullptr;       // two-pass column-reduction scratch (own per net: the DeepONet
   float* narrow_part = nullptr;  // nets run on two streams), narrow-input weight-gradient partials
   float* gl_part = nullptr;      // K-split weight-gradient partials
+  float* mw_part = nullptr;      // row-segment partials of the masked weight gradient
 };
 
 struct DevBuf {
@@ -463,7 +473,24 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
       st = N.ws;
     }
     float* cs_i = ov ? N.cs[i % 3] : N.colsum;  // this layer's bias partials
-    if (L.any_active && is_narrow(L)) {
+    if (L.any_active && L.mwg) {  // masked weight gradient (entries of the mask only, bias included)
+      const int id = prof_begin(x, st);
+      const int64_t nchunk = (L.rows + MW_R - 1) / MW_R;
+      const int64_t seg_rows = ((nchunk + L.mw_seg - 1) / L.mw_seg) * MW_R;
+      float* out = L.mw_seg > 1 ? N.mw_part : N.gl;
+      mw_kernel(L.n_out, L.n_in)<<<dim3((unsigned)(L.mw_seg * L.mw_tb), N.nch), MW_NT, mw_smem_bytes(L.n_out, L.n_in), st>>>(
+          G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, L.n_in, L.mw_seg, seg_rows, L.mw, out,
+          (int64_t)N.nch * x->k, x->k, x->sq);
+      x->launches++;
+      if (L.mw_seg > 1) {  // fixed-order sum of the row segments' partials
+        k_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((L.mw_hi - L.mw_lo + 255) / 256, 256)), N.nch),
+                          256, 0, st>>>(N.mw_part, L.mw_seg, (int64_t)N.nch * x->k, x->k, L.mw_lo, L.mw_hi, N.gl);
+        x->launches++;
+      }
+      const double fl = 2.0 * N.nch * L.rows * (double)L.mw_pairs;
+      x->flop_acc += fl;
+      prof_end(x, id, st, "mask_wgrad", fl, 4.0 * N.nch * L.rows * (double)(L.n_out + L.n_in));
+    } else if (L.any_active && is_narrow(L)) {
       const int id = prof_begin(x, st);
       launch_wgrad_narrow(x, L, G, in, s_in, st);
       const double fl = 2.0 * N.nch * L.rows * L.n_out * (double)(L.n_in + 1);
@@ -540,7 +567,7 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         pre.only = L.planes_only;
       }
       float* cs_prev = ov ? N.cs[(i - 1) % 3] : N.colsum;
-      if (Pv.bias_active && cs_prev) { a.colsum = cs_prev; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
+      if (Pv.bias_active && !Pv.mwg && cs_prev) { a.colsum = cs_prev; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
       N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
       cur = nxt;
     }
@@ -1314,6 +1341,212 @@ void set_rec(hmc_ctx* x, float* samples, uint8_t* acc, double* dH, int64_t S, in
 }
 
 // ---------------------------------------------------------------------------------------------
+// Masked weight gradient (masked_wgrad.cuh): per hidden layer, the active entries grouped into
+// tasks of <= MW_G entries of one output row, and the choice against the dense weight-gradient
+// GEMM by a cost model (DESIGN.md §5 "masked weight gradient"):
+//   dense GEMM : 2 nch rows n_out n_in FLOP at ~140 TFLOP/s (3xTF32 engine, measured cfg5) + 5 us
+//   masked     : shared-memory words nch rows (T + |mask|) (T tasks) at 32 words / clk
+//                / SM x 0.7, or the operand bytes at 6 TB/s, whichever is larger, x wave
+//                quantisation, + 3 us (+ 3 us for the segment reduction)
+// Row segments: the count with the fewest chunk-times per resident CTA slot (2 per SM).
+void plan_masked_wgrad(hmc_ctx* x, const std::vector<int32_t>& slot, std::string& err) {
+  // hmc_debug_set_engine(4) (tests) or HMC_MWG=1 (make DEV=1): wherever the kernel applies;
+  // hmc_debug_set_engine(2) or HMC_MWG=0: never
+  int force = engine_override() == 4 ? 1 : (engine_override() == 2 ? 0 : -1);
+  if (const char* f = dev_env("HMC_MWG")) force = atoi(f);
+  const int sms = x->tc.num_sms > 0 ? x->tc.num_sms : 148;
+  bool any = false;
+  for (int ni = 0; ni < x->n_nets; ++ni) {
+    NetInfo& N = x->nets[ni];
+    size_t part_cap = 0;
+    for (int li = N.l_min < 0 ? (int)N.layers.size() : N.l_min; li < (int)N.layers.size(); ++li) {
+      LayerInfo& L = x->layers[N.layers[li]];
+      const bool mlp_out = (x->kind == HMC_MLP && li == (int)N.layers.size() - 1);
+      if (mlp_out || !L.any_active || is_narrow(L) || L.n_in % 4 || L.n_out % 4 || L.n_in > MW_MAXW ||
+          L.n_out > MW_MAXW || L.act == ACT_SIN || force == 0)
+        continue;
+      // tasks: the active entries of each output row (bias = input column n_in), MW_G at a time
+      std::vector<std::vector<int>> tasks;
+      std::vector<int> tasks_o;
+      int64_t npairs = 0, lo = INT64_MAX, hi = -1;
+      for (int o = 0; o < L.n_out; ++o) {
+        std::vector<int> cur;
+        auto note = [&](int32_t sl) { lo = std::min<int64_t>(lo, sl); hi = std::max<int64_t>(hi, sl + 1); ++npairs; };
+        for (int i = 0; i <= L.n_in; ++i) {
+          const int32_t sl = (i < L.n_in) ? slot[L.w_off + (int64_t)o * L.n_in + i] : (L.bias ? slot[L.b_off + o] : -1);
+          if (sl < 0) continue;
+          note(sl);
+          cur.push_back(i);
+          if ((int)cur.size() == MW_G) { tasks.push_back(cur); tasks_o.push_back(o); cur.clear(); }
+        }
+        if (!cur.empty()) { tasks.push_back(cur); tasks_o.push_back(o); }
+      }
+      const int T = (int)tasks.size();
+      if (T == 0) continue;
+      const int n_tb = (T + MW_NT - 1) / MW_NT;
+      // row segments
+      const int64_t rows = L.rows, nch = N.nch;
+      const int64_t nchunk = (rows + MW_R - 1) / MW_R;
+      const int64_t slots = 2LL * sms;
+      int best_s = 1;
+      double best_c = 1e300;
+      const bool contiguous = (hi - lo == npairs);
+      for (int s = 1; s <= std::min<int64_t>(64, nchunk); ++s) {
+        if (s > 1 && !contiguous) break;
+        const double c = (double)((nch * n_tb * s + slots - 1) / slots) * (double)((nchunk + s - 1) / s) + (s > 1 ? 2.0 : 0.0);
+        if (c < best_c - 1e-9) { best_c = c; best_s = s; }
+      }
+      // lanes.  Warps of 32 tasks with distinct o mod 32 (conflict-free G loads), filled
+      // largest task first into the warp whose input-column residues (i mod 32) stay the most
+      // balanced; then each warp's lane x residue multigraph is edge-coloured (bipartite: as many
+      // colours as its largest degree, Koenig) and an entry's colour is its position p, so at
+      // every p the lanes read distinct banks of X.  Unused positions read a zero column whose
+      // bank is free at that position (k-slot -1: not written back).
+      const int pad0 = L.n_in + 1;  // zero columns n_in + 1 .. n_in + 3 (n_in: the ones)
+      std::vector<int> ord(T);
+      for (int t = 0; t < T; ++t) ord[t] = t;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return tasks[a].size() > tasks[b].size(); });
+      std::vector<std::vector<int>> warps;
+      for (int nwarp = (T + 31) / 32; warps.empty(); ++nwarp) {
+        std::vector<std::vector<int>> W(nwarp);
+        std::vector<uint32_t> used(nwarp, 0);
+        std::vector<std::array<int, 32>> deg(nwarp);
+        for (auto& d : deg) d.fill(0);
+        bool ok = true;
+        for (int t : ord) {
+          const uint32_t bit = 1u << (tasks_o[t] & 31);
+          int best = -1;
+          long long bkey = 0;
+          for (int w = 0; w < nwarp; ++w) {
+            if (W[w].size() >= 32 || (used[w] & bit)) continue;
+            std::array<int, 32> d = deg[w];
+            for (int i : tasks[t]) ++d[i & 31];
+            int mx = 0;
+            long long sq = 0;
+            for (int v : d) { mx = std::max(mx, v); sq += (long long)v * v; }
+            const long long key = ((long long)mx << 40) + (sq << 8) + (long long)W[w].size();
+            if (best < 0 || key < bkey) { best = w; bkey = key; }
+          }
+          if (best < 0) { ok = false; break; }
+          W[best].push_back(t);
+          used[best] |= bit;
+          for (int i : tasks[t]) ++deg[best][i & 31];
+        }
+        if (ok) warps = W;
+      }
+      const int Tp = 32 * (int)warps.size();  // lanes incl. idle ones
+      std::vector<int32_t> info(Tp, 0);
+      std::vector<int16_t> pi((size_t)MW_G * Tp, (int16_t)pad0);
+      std::vector<int32_t> ps((size_t)MW_G * Tp, -1);
+      for (int w = 0; w < (int)warps.size(); ++w) {
+        const int nl = (int)warps[w].size();
+        // edges: (lane, residue) per entry
+        std::vector<int> el, er, ei, col;
+        for (int l = 0; l < nl; ++l)
+          for (int i : tasks[warps[w][l]]) { el.push_back(l); er.push_back(i & 31); ei.push_back(i); }
+        const int E = (int)el.size();
+        int D = 0;
+        {
+          std::array<int, 32> dl{}, dr{};
+          for (int e = 0; e < E; ++e) { D = std::max(D, ++dl[el[e]]); D = std::max(D, ++dr[er[e]]); }
+        }
+        std::vector<int> cl((size_t)32 * D, -1), cr((size_t)32 * D, -1);  // [vertex][colour] -> edge
+        col.assign(E, -1);
+        for (int e = 0; e < E; ++e) {
+          const int l = el[e], r = er[e];
+          int a = 0, b = 0;
+          while (cl[l * D + a] >= 0) ++a;
+          while (cr[r * D + b] >= 0) ++b;
+          if (cr[r * D + a] >= 0) {  // flip the a/b alternating path from r (never reaches l)
+            std::vector<int> path;
+            int v = r, c = a;
+            bool right = true;
+            for (;;) {
+              const int f = right ? cr[v * D + c] : cl[v * D + c];
+              if (f < 0) break;
+              path.push_back(f);
+              v = right ? el[f] : er[f];
+              right = !right;
+              c = (c == a) ? b : a;
+            }
+            for (int f : path) { cl[el[f] * D + col[f]] = -1; cr[er[f] * D + col[f]] = -1; }
+            for (int f : path) {
+              col[f] = (col[f] == a) ? b : a;
+              cl[el[f] * D + col[f]] = f;
+              cr[er[f] * D + col[f]] = f;
+            }
+          }
+          col[e] = a;
+          cl[l * D + a] = e;
+          cr[r * D + a] = e;
+        }
+        if (D > MW_G) {  // (more colours than positions: first-come positions, bank conflicts accepted)
+          std::array<int, 32> nxt{};
+          for (int e = 0; e < E; ++e) col[e] = nxt[el[e]]++;
+        }
+        std::vector<int> cnt(nl, 0);
+        for (int e = 0; e < E; ++e) {
+          const int l = el[e], p = col[e], i = ei[e];
+          const int o = tasks_o[warps[w][l]];
+          const size_t q = (size_t)p * Tp + 32 * w + l;
+          pi[q] = (int16_t)i;
+          ps[q] = (i < L.n_in) ? slot[L.w_off + (int64_t)o * L.n_in + i] : slot[L.b_off + o];
+          cnt[l] = std::max(cnt[l], p + 1);
+        }
+        // unused positions of busy lanes: a zero column in a bank no entry uses at that position
+        for (int p = 0; p < MW_G; ++p) {
+          uint32_t busy = 0;
+          for (int l = 0; l < nl; ++l)
+            if (ps[(size_t)p * Tp + 32 * w + l] >= 0) busy |= 1u << (pi[(size_t)p * Tp + 32 * w + l] & 31);
+          int z = pad0;
+          for (int j = 0; j < 3; ++j)
+            if (!(busy >> ((pad0 + j) & 31) & 1u)) { z = pad0 + j; break; }
+          for (int l = 0; l < 32; ++l)
+            if (ps[(size_t)p * Tp + 32 * w + l] < 0) pi[(size_t)p * Tp + 32 * w + l] = (int16_t)z;
+        }
+        for (int l = 0; l < nl; ++l) info[32 * w + l] = tasks_o[warps[w][l]] | (cnt[l] << 16);
+      }
+      {  // cost: shared-memory wavefronts per row = sum over warps of (1 + its positions)
+        double wf = 0;
+        for (int w = 0; w < (int)warps.size(); ++w) {
+          int nw = 0;
+          for (int l = 0; l < 32; ++l) nw = std::max(nw, info[32 * w + l] >> 16);
+          wf += 1 + nw;
+        }
+        const int tb = (Tp + MW_NT - 1) / MW_NT;
+        const double ideal = (double)nch * tb * nchunk / slots;  // chunk-times at perfect balance
+        const double quant = std::max(1.0, best_c / std::max(ideal, 1e-9));
+        const double t_smem = (double)nch * rows * wf / (sms * 1.8e9 * 0.45);
+        const double t_hbm = (double)nch * rows * (L.n_out + L.n_in) * 4.0 / 6e12;
+        const double t_mw = std::max(t_smem, t_hbm) * quant + 3e-6 + (best_s > 1 ? 3e-6 : 0.0);
+        const double t_tc = 2.0 * nch * rows * L.n_out * (double)L.n_in / (x->tc.enabled ? 140e12 : 30e12) + 5e-6;
+        if (!(force == 1 || t_mw < t_tc)) continue;
+      }
+      int32_t* d_info = dalloc<int32_t>(x, Tp, err);
+      int16_t* d_pi = dalloc<int16_t>(x, pi.size(), err);
+      int32_t* d_ps = dalloc<int32_t>(x, ps.size(), err);
+      CK(cudaMemcpy(d_info, info.data(), Tp * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_pi, pi.data(), pi.size() * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_ps, ps.data(), ps.size() * 4, cudaMemcpyHostToDevice));
+      L.mwg = true;
+      L.mw = MwTasks{d_info, d_pi, d_ps, Tp};
+      L.mw_seg = best_s;
+      L.mw_tb = (Tp + MW_NT - 1) / MW_NT;
+      L.mw_lo = lo;
+      L.mw_hi = hi;
+      L.mw_pairs = npairs;
+      if (best_s > 1) part_cap = std::max(part_cap, (size_t)best_s * nch * x->k);
+      any = true;
+    }
+    if (part_cap) N.mw_part = dalloc<float>(x, part_cap, err);
+  }
+  if (any)
+    for (auto& L : x->layers)
+      if (L.mwg)
+        CK(cudaFuncSetAttribute(mw_kernel(L.n_out, L.n_in), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)mw_smem_bytes(MW_MAXW, MW_MAXW)));
+}
+
 void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hmc_config* cfg, std::string& err,
                 bool allow_narrow = true) {
   CFG(arch && data && cfg, "arch, data and config must be non-NULL");
@@ -1728,6 +1961,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       }
     }
   }
+  plan_masked_wgrad(x, slot, err);
   CK(cudaMallocHost((void**)&x->h_rec, sizeof(Rec)));
   CK(cudaMallocHost((void**)&x->h_eps, sizeof(double)));
   CK(cudaEventCreateWithFlags(&x->ev_stage, cudaEventDisableTiming));
@@ -1761,6 +1995,11 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
                               " blocks of " + std::to_string(x->nwa.rb) + " rows, " + std::to_string(x->nwa.nblk) +
                               " blocks, hw " + std::to_string(x->nw_hw) + ")"
                         : x->tc.describe();
+  {
+    int nm = 0, na = 0;
+    for (auto& L : x->layers) { nm += L.mwg; na += L.any_active && !is_narrow(L); }
+    if (nm) x->engine += " + masked wgrad (" + std::to_string(nm) + " of " + std::to_string(na) + " layers)";
+  }
   CK(cudaDeviceSynchronize());
 }
 
@@ -2354,9 +2593,9 @@ int hmc_debug_xb_permute(int32_t dir, int32_t C, int32_t G, int64_t n_loc, int32
 }
 
 int hmc_debug_set_engine(int32_t mode) {
-  if (mode < 0 || mode > 3) {
-    g_err = "config: engine mode must be 0 (automatic), 1 (per-layer SIMT only), 2 (per-layer engines) or 3 "
-            "(narrow engine in cluster mode only)";
+  if (mode < 0 || mode > 4) {
+    g_err = "config: engine mode must be 0 (automatic), 1 (per-layer SIMT only), 2 (per-layer engines), 3 "
+            "(narrow engine in cluster mode only) or 4 (masked weight gradient wherever it applies)";
     return HMC_E_CONFIG;
   }
   engine_override() = mode;
