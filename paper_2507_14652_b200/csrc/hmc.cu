@@ -70,12 +70,20 @@ struct NetInfo {
   int64_t rows = 0;
   const float* input = nullptr;
   int max_w = 0;
-  float* G[3] = {nullptr, nullptr, nullptr};  // gradient buffers (3 rotate when wgrads run on ws)
+  // gradient buffers: with overlapped weight gradients, nrot of them rotate (one per layer of the
+  // net, >= 3), so no input-gradient GEMM waits for a weight gradient to release its delta
+  static constexpr int MAXROT = 8;
+  float* G[MAXROT] = {};
+  int nrot = 2;
   float* colsum = nullptr;  // [C x ceil(rows/32) x max_w] fused bias-gradient partials (layer top)
-  float* cs[3] = {nullptr, nullptr, nullptr};  // per-layer rotation of colsum (cs[i % 3] = layer i)
+  float* cs[MAXROT] = {};   // per-layer rotation of colsum (cs[i % nrot] = layer i)
   // weight gradients on their own captured stream ws, overlapping the input-gradient chain:
   // evA[i] = delta_i (and its bias partials) ready, evW[i] = wgrad(i) done
   cudaStream_t ws = nullptr;
+  cudaStream_t ws2 = nullptr;  // second weight-gradient stream: layers alternate between ws / ws2, so
+                               // wgrad(i - 1) need not wait for wgrad(i) (their outputs - k-slot
+                               // ranges, partial buffers - are disjoint; colred has a copy per stream)
+  float* colred2 = nullptr;
   std::vector<cudaEvent_t> evA, evW;
   bool cs_ready = false;    // colsum holds the partials of the current G
   // the chains this net runs for (POINTS_XC: the branch runs only this rank's chain block) and the
@@ -236,6 +244,7 @@ struct hmc_ctx {
       for (auto e : N.evA) cudaEventDestroy(e);
       for (auto e : N.evW) cudaEventDestroy(e);
       if (N.ws) cudaStreamDestroy(N.ws);
+      if (N.ws2) cudaStreamDestroy(N.ws2);
     }
     if (st) cudaStreamDestroy(st);
   }
@@ -459,20 +468,23 @@ void enqueue_forward_hidden(hmc_ctx* x, NetInfo& N, int i, cudaStream_t st) {
 void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t ms) {
   // ws: the weight-gradient stream (N.ws, when this net's backward runs with overlap) - wgrad(i)
   // starts when delta_i is ready (evA[i]) and runs beside dgrad(i) and dgrad(i - 1); dgrad(i)
-  // writes the gradient / bias-partial buffers last read by wgrad(i + 2), so it waits for evW[i + 2]
-  const bool ov = N.ws != nullptr && N.G[2] != nullptr && (int)N.evA.size() > top && !x->prof_armed;
+  // writes the gradient / bias-partial buffers last read by wgrad(i + nrot - 1) (never, when nrot covers the net)
+  const bool ov = N.ws != nullptr && N.nrot >= 3 && (int)N.evA.size() > top && !x->prof_armed;
   for (int i = top; i >= N.l_min; --i) {
     LayerInfo& L = x->layers[N.layers[i]];
     const float* G = N.G[cur];
     int64_t s_in;
     const float* in = layer_input(x, N, i, &s_in);
     cudaStream_t st = ms;
+    const bool alt = ov && N.ws2 && (i & 1);
+    float* colred = alt ? N.colred2 : N.colred;
     if (ov) {
+      cudaStream_t wsi = alt ? N.ws2 : N.ws;
       cudaEventRecord(N.evA[i], ms);
-      cudaStreamWaitEvent(N.ws, N.evA[i], 0);
-      st = N.ws;
+      cudaStreamWaitEvent(wsi, N.evA[i], 0);
+      st = wsi;
     }
-    float* cs_i = ov ? N.cs[i % 3] : N.colsum;  // this layer's bias partials
+    float* cs_i = ov ? N.cs[i % N.nrot] : N.colsum;  // this layer's bias partials
     if (L.any_active && L.mwg) {  // masked weight gradient (entries of the mask only, bias included)
       const int id = prof_begin(x, st);
       const int64_t nchunk = (L.rows + MW_R - 1) / MW_R;
@@ -535,8 +547,8 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
           } else {
             const int chunks = (int)((L.rows + COLRED_CH - 1) / COLRED_CH);
             k_colred_p1<<<dim3(chunks, N.nch), 256, 0, st>>>(nullptr, G, L.rows * L.n_out, L.rows, L.n_out,
-                                                              N.colred, chunks, x->sq);
-            k_colred_p2<<<N.nch, 256, 0, st>>>(N.colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, N.gl, x->k);
+                                                              colred, chunks, x->sq);
+            k_colred_p2<<<N.nch, 256, 0, st>>>(colred, chunks, L.n_out, x->d_slot + L.b_off, nullptr, N.gl, x->k);
             x->launches += 2;
           }
           prof_end(x, id2, st, "bias_grad", 1.0 * N.nch * L.rows * L.n_out, 4.0 * N.nch * L.rows * L.n_out);
@@ -549,11 +561,11 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
                  4.0 * a.batch * ((double)a.M * a.K + (double)a.K * a.N));
       }
     }
-    if (ov) cudaEventRecord(N.evW[i], N.ws);
+    if (ov) cudaEventRecord(N.evW[i], st);
     if (i > N.l_min) {
       st = ms;
-      const int nxt = ov ? (cur + 1) % 3 : (cur ^ 1);
-      if (ov && i + 2 <= top) cudaStreamWaitEvent(ms, N.evW[i + 2], 0);  // buffers of delta_{i+2}
+      const int nxt = ov ? (cur + 1) % N.nrot : (cur ^ 1);
+      if (ov && i + N.nrot - 1 <= top) cudaStreamWaitEvent(ms, N.evW[i + N.nrot - 1], 0);  // buffers of delta_{i+nrot-1}
       const LayerInfo& Pv = x->layers[N.layers[i - 1]];
       GemmArgs a = gemm_base((int)L.rows, L.n_in, L.n_out, N.nch);
       a.A = G; a.lda = L.n_out; a.sA = L.rows * L.n_out;
@@ -566,13 +578,16 @@ void enqueue_backward_net(hmc_ctx* x, NetInfo& N, int top, int cur, cudaStream_t
         pre.hi = N.whi + L.q_off; pre.lo = N.wlo ? N.wlo + L.q_off : nullptr; pre.ld = L.n_in; pre.stride = x->Ptc;
         pre.only = L.planes_only;
       }
-      float* cs_prev = ov ? N.cs[(i - 1) % 3] : N.colsum;
+      float* cs_prev = ov ? N.cs[(i - 1) % N.nrot] : N.colsum;
       if (Pv.bias_active && !Pv.mwg && cs_prev) { a.colsum = cs_prev; a.s_colsum = (int64_t)((Pv.rows + 31) / 32) * Pv.n_out; }
       N.cs_ready = launch_gemm(x, a, true, false, st, "dgrad", L.tc_w ? &pre : nullptr) && a.colsum;
       cur = nxt;
     }
   }
-  if (ov) cudaStreamWaitEvent(ms, N.evW[N.l_min], 0);  // all weight gradients done (stream order)
+  if (ov) {  // all weight gradients done (stream order on each of ws / ws2)
+    cudaStreamWaitEvent(ms, N.evW[N.l_min], 0);
+    if (N.ws2 && N.l_min + 1 <= top) cudaStreamWaitEvent(ms, N.evW[N.l_min + 1], 0);
+  }
 }
 
 // POINTS_XB pieces: the all-gather result xb_recv ([rank][chain][i][k]) ordered
@@ -1917,6 +1932,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       cap = std::max(cap, chunks * (size_t)(x->nets[ni].max_w + 1));
     }
     for (int ni = 0; ni < x->n_nets; ++ni) x->nets[ni].colred = dalloc<float>(x, (size_t)C * cap, err);
+    if (x->wgrad_ov)
+      for (int ni = 0; ni < x->n_nets; ++ni) x->nets[ni].colred2 = dalloc<float>(x, (size_t)C * cap, err);
   }
   {  // narrow-input weight-gradient partials: max over narrow layers of chunks x n_out x (n_in + 1)
     size_t cap = 0;
@@ -1944,14 +1961,16 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       N.G[0] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       N.G[1] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
       if (x->tc.enabled) N.colsum = dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err);
-      if (x->wgrad_ov) {  // overlapped weight gradients: a third gradient buffer, rotated partials
-        N.G[2] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
+      if (x->wgrad_ov) {  // overlapped weight gradients: one gradient buffer per layer, rotated partials
+        N.nrot = std::min(NetInfo::MAXROT, std::max(3, nl));
+        for (int r = 2; r < N.nrot; ++r) N.G[r] = dalloc<float>(x, (size_t)C * N.rows * N.max_w, err);
         const int top = nl - 1;
-        for (int r = 0; r < 3; ++r)
-          N.cs[r] = (r == top % 3) ? N.colsum
+        for (int r = 0; r < N.nrot; ++r)
+          N.cs[r] = (r == top % N.nrot) ? N.colsum
                                    : (x->tc.enabled ? dalloc<float>(x, (size_t)C * ((N.rows + 31) / 32) * N.max_w, err)
                                                     : nullptr);
         CK(cudaStreamCreateWithFlags(&N.ws, cudaStreamNonBlocking));
+        if (!(dev_env("HMC_WS2") && atoi(dev_env("HMC_WS2")) == 0)) CK(cudaStreamCreateWithFlags(&N.ws2, cudaStreamNonBlocking));
         N.evA.resize(nl);
         N.evW.resize(nl);
         for (int i = 0; i < nl; ++i) {
