@@ -670,6 +670,43 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     LayerInfo& O = x->layers[N.layers[nl - 1]];
     int64_t s_in;
     const float* in = layer_input(x, N, nl - 1, &s_in);
+    // one pass over the output layer's input: forward, residual, likelihood partials, output-layer
+    // gradient partials and the rank-1 input gradient (k_out_fused), when its conditions hold
+    const bool back = nl - 1 > N.l_min;
+    const int pv_act = back ? x->layers[N.layers[nl - 2]].act : ACT_ID;
+    if (!x->sq && N.l_min >= 0 && O.n_in <= 256 && (pv_act == ACT_TANH || pv_act == ACT_ID) &&
+        !(dev_env("HMC_OUT_FUSED") && atoi(dev_env("HMC_OUT_FUSED")) == 0)) {
+      const int id = prof_begin(x, st);
+      dim3 grid((unsigned)x->colred_chunks, C);
+      float* G = back ? N.G[0] : nullptr;
+      // bias partials of layer nl - 2 into the buffer enqueue_backward_net hands its weight gradient
+      const int top = nl - 2;
+      const bool ov = N.ws != nullptr && N.nrot >= 3 && (int)N.evA.size() > top && !x->prof_armed;
+      float* cs = back && x->layers[N.layers[top]].bias_active ? (ov ? N.cs[top % N.nrot] : N.colsum) : nullptr;
+      const int64_t s_cs = (int64_t)((O.rows + 31) / 32) * O.n_in;
+#define OF(MO_) k_out_fused<MO_><<<grid, 256, 0, st>>>(in, s_in, O.n_in, O.rows, x->Wd, x->P, O.w_off, O.b_off, x->d_y, \
+                                                      x->R, 1.0 / (x->sigma * x->sigma), x->part_sq, x->n_part,       \
+                                                      N.colred, x->colred_chunks, G, pv_act, cs, s_cs)
+      if (O.n_in <= 32) OF(1);
+      else if (O.n_in <= 64) OF(2);
+      else if (O.n_in <= 128) OF(4);
+      else OF(8);
+#undef OF
+      x->launches++;
+      const double fl = 2.0 * C * O.rows * O.n_in * (back ? 3.0 : 2.0);
+      x->flop_acc += fl;
+      prof_end(x, id, st, "out_fused", fl, 4.0 * C * O.rows * O.n_in * (back ? 2.0 : 1.0));
+      if (O.any_active) {
+        k_colred_p2<<<C, 256, 0, st>>>(N.colred, x->colred_chunks, O.n_in, x->d_slot + O.w_off,
+                                       O.bias ? x->d_slot + O.b_off : nullptr, x->gl, x->k);
+        x->launches++;
+      }
+      if (back) {
+        N.cs_ready = cs != nullptr;
+        enqueue_backward_net(x, N, nl - 2, 0, st);
+      }
+      return;
+    }
     {
       const int id = prof_begin(x, st);
       dim3 grid(x->n_part, C);

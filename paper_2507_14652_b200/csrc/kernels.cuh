@@ -132,6 +132,97 @@ __global__ void __launch_bounds__(256) k_out_fwd(const float* __restrict__ Ain, 
   if (threadIdx.x == 0) part_sq[(int64_t)c * n_part + blockIdx.x] = tot;
 }
 
+// ---- the MLP output layer in ONE pass over its input A (training mode; tanh / identity below it):
+//      f = A w + b, r = y - f, R = r / sigma^2, fp64 sum r^2 per 64-row block, the weight-
+//      and bias-gradient partials of the output layer per 256-row chunk (part[c][chunk][j] =
+//      sum_n R[n] A[n][j], j = n_in: sum_n R[n]; reduced by k_colred_p2) and, when the backward
+//      continues, the input gradient G[n][j] = R[n] w[j] act'(A[n][j]).  Every step is row-local
+//      once R[n] is known, so A (the largest activation) is read once instead of three times; the
+//      input gradient's column sums per 32-row block (the next layer's bias-gradient partials, in
+//      the layout of the tcgen05 input-gradient epilogue's) come with it.
+//      CTA = 256 rows (8 warps x 32 rows); lane j-slots j = lane + 32 m (m < MO, n_in <= 32 MO);
+//      column partials: each warp over its rows in order, then the warps in order (fixed order).
+template <int MO>
+__global__ void __launch_bounds__(256) k_out_fused(const float* __restrict__ Ain, int64_t sA, int n_in, int64_t rows,
+                                                   const float* __restrict__ Wd, int64_t P, int64_t w_off,
+                                                   int64_t b_off, const float* __restrict__ y, float* __restrict__ R,
+                                                   double inv_s2, double* __restrict__ part_sq, int n_part,
+                                                   float* __restrict__ colpart, int n_chunks, float* __restrict__ G,
+                                                   int act, float* __restrict__ cs, int64_t s_cs) {
+  __shared__ float wp[8][32 * MO + 1];  // per-warp column partials (j = n_in: sum R)
+  __shared__ double red[8];
+  const int c = blockIdx.y, ch = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* w = Wd + (int64_t)c * P + w_off;
+  float wr[MO];
+#pragma unroll
+  for (int m = 0; m < MO; ++m) wr[m] = (lane + 32 * m < n_in) ? __ldg(w + lane + 32 * m) : 0.f;
+  const float bias = (b_off >= 0) ? __ldg(Wd + (int64_t)c * P + b_off) : 0.f;
+  const float* A = Ain + (int64_t)c * sA;
+  float cp[MO];
+#pragma unroll
+  for (int m = 0; m < MO; ++m) cp[m] = 0.f;
+  float gsum[MO];  // bias-gradient partials of the layer below: sum of G over this warp's 32-row block
+#pragma unroll
+  for (int m = 0; m < MO; ++m) gsum[m] = 0.f;
+  float rsum = 0.f;
+  double psq = 0.0;
+  const int64_t n0 = (int64_t)ch * 256 + warp * 32;
+  for (int rr = 0; rr < 32; ++rr) {
+    const int64_t n = n0 + rr;
+    if (n >= rows) break;
+    float a[MO];
+    float s = 0.f;
+#pragma unroll
+    for (int m = 0; m < MO; ++m) {
+      a[m] = (lane + 32 * m < n_in) ? A[n * n_in + lane + 32 * m] : 0.f;
+      s = fmaf(a[m], wr[m], s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float r = y[n] - (s + bias);
+    const float Rn = (float)((double)r * inv_s2);
+    psq += (double)r * (double)r;
+    if (lane == 0) R[(int64_t)c * rows + n] = Rn;
+    rsum += Rn;
+#pragma unroll
+    for (int m = 0; m < MO; ++m) {
+      cp[m] = fmaf(Rn, a[m], cp[m]);
+      if (G && lane + 32 * m < n_in) {
+        float v = Rn * wr[m];
+        if (act == ACT_TANH) v *= (1.f - a[m] * a[m]);
+        G[((int64_t)c * rows + n) * n_in + lane + 32 * m] = v;
+        gsum[m] += v;
+      }
+    }
+  }
+  if (G && cs && n0 < rows) {  // (the 32-row block partials the weight-gradient GEMM's bias fusion reads)
+    const int64_t blk = n0 / 32;
+#pragma unroll
+    for (int m = 0; m < MO; ++m)
+      if (lane + 32 * m < n_in) cs[(int64_t)c * s_cs + blk * n_in + lane + 32 * m] = gsum[m];
+  }
+#pragma unroll
+  for (int m = 0; m < MO; ++m) wp[warp][lane + 32 * m] = cp[m];
+  if (lane == 0) {
+    wp[warp][32 * MO] = rsum;
+    red[warp] = psq;  // (lane-local: every lane of the warp holds the same sum r^2)
+  }
+  __syncthreads();
+  float* pc = colpart + ((int64_t)c * n_chunks + ch) * (n_in + 1);
+  for (int j = threadIdx.x; j <= n_in; j += 256) {
+    const int jj = j < n_in ? j : 32 * MO;
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += wp[q][jj];
+    pc[j] = t;
+  }
+  if (threadIdx.x < 4) {  // sum r^2 of each 64-row block: warps 2 b, 2 b + 1
+    const int64_t blk = (int64_t)ch * 4 + threadIdx.x;
+    if (blk < n_part) part_sq[(int64_t)c * n_part + blk] = red[2 * threadIdx.x] + red[2 * threadIdx.x + 1];
+  }
+}
+
 // ---- input gradient of the width-1 output layer: G[n, j] = R[n] w[j] act'(A[n, j]) ----
 __global__ void k_rank1_dact(const float* __restrict__ R, const float* __restrict__ Wd, int64_t P,
                              int64_t w_off, const float* __restrict__ Aprev, const float* __restrict__ Dprev,

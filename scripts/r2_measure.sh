@@ -27,5 +27,14 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
   -o $O/full_cfg5_fwd python bench.py --cfg cfg5 --steps 1 --warmup 3 --L 2 --eps 4e-7 --no-e2e --no-cpu-baseline > $O/ncu_full2.log 2>&1; echo full2 rc=$?
 ncu --set full --clock-control none --import-source on -k regex:k_narrow -s 3 -c 1 \
   -o $O/full_cfg2_narrow python bench.py --cfg cfg2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_full3.log 2>&1; echo full3 rc=$?
+ncu --set full --clock-control none --import-source on -k regex:k_narrow -s 3 -c 1 \
+  -o $O/full_cfg1_narrow python bench.py --cfg cfg1 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_full4.log 2>&1; echo full4 rc=$?
 fi
 ls -la $O | tail -40
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB copy-back limit): profile text /
+# bench lines under $O/prof, the per-class traffic csv kept, the reports deleted but the weight-gradient one
+mkdir -p $O/prof
+R2_DIR=$O R2_OUT=$O/prof python scripts/r2_profiles.py > $O/prof/summary.log 2>&1; echo summary rc=$?
+python scripts/ncu_traffic.py $O/traffic_cfg5.csv > $O/prof/traffic.log 2>&1; cp /tmp/traffic_agg.json $O/prof/ 2>/dev/null
+rm -f $O/full_cfg5_fwd.ncu-rep $O/full_cfg2_narrow.ncu-rep $O/full_cfg1_narrow.ncu-rep
+du -sh gpurun_out

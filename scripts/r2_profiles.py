@@ -8,8 +8,8 @@ import os
 import subprocess
 import sys
 
-R = "gpurun_out/r2"
-OUT = "profiles"
+R = os.environ.get("R2_DIR", "gpurun_out/r2")
+OUT = os.environ.get("R2_OUT", "profiles")
 UNIT = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 
 
@@ -47,7 +47,8 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__cluster_size",
-        "smsp__inst_executed.sum", "sm__cycles_active.avg"]
+        "smsp__inst_executed.sum", "sm__cycles_active.avg", "dram__bytes_read.sum.per_second",
+        "dram__bytes_write.sum.per_second"]
 
 
 def full(rep, title):
@@ -97,7 +98,8 @@ if __name__ == "__main__":
             lines += launches(c) + [""]
     for rep, title in [(f"{R}/full_cfg5_wgrad.ncu-rep", "cfg5 weight-gradient GEMM (EPI_WGRAD), 64 chains"),
                        (f"{R}/full_cfg5_fwd.ncu-rep", "cfg5 forward GEMM (EPI_FWD, pre-split weights), 64 chains"),
-                       (f"{R}/full_cfg2_narrow.ncu-rep", "cfg2 narrow-engine kernel (one launch = all L = 50 steps)")]:
+                       (f"{R}/full_cfg2_narrow.ncu-rep", "cfg2 narrow-engine kernel (one launch = all L = 50 steps)"),
+                       (f"{R}/full_cfg1_narrow.ncu-rep", "cfg1 narrow-engine kernel (one launch = all L = 20 steps)")]:
         if os.path.exists(rep):
             lines += full(rep, title) + [""]
     open(f"{OUT}/r02_ncu_summary.txt", "w").write("\n".join(lines) + "\n")
