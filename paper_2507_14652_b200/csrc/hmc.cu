@@ -411,12 +411,18 @@ void launch_fwd_narrow(hmc_ctx* x, const LayerInfo& L, const float* in, int64_t 
   x->launches++;
 }
 
+// rows per CTA of the narrow-input weight gradient: the long chunk when it leaves >= 8 CTAs per SM
+inline int narrow_wrows(int64_t rows, int nch) {
+  return ((rows + NARROW_WROWS - 1) / NARROW_WROWS) * nch >= 8 * 148 ? NARROW_WROWS : NARROW_ROWS;
+}
+
 void launch_wgrad_narrow(hmc_ctx* x, const LayerInfo& L, const float* G, const float* in, int64_t s_in,
                          cudaStream_t st) {
   const NetInfo& N = x->nets[L.net];
-  const int nch = (int)((L.rows + NARROW_ROWS - 1) / NARROW_ROWS);
+  const int wrows = narrow_wrows(L.rows, N.nch);
+  const int nch = (int)((L.rows + wrows - 1) / wrows);
   dim3 grid(nch, N.nch);
-#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->nets[L.net].narrow_part, nch, x->sq)
+#define WN(DIN_) k_wgrad_narrow_p1<DIN_><<<grid, 256, 0, st>>>(G, L.rows * L.n_out, in, s_in, L.rows, L.n_out, x->nets[L.net].narrow_part, nch, x->sq, wrows)
   switch (L.n_in) {
     case 1: WN(1); break; case 2: WN(2); break; case 3: WN(3); break; case 4: WN(4); break;
     case 5: WN(5); break; case 6: WN(6); break; case 7: WN(7); break; default: WN(8); break;

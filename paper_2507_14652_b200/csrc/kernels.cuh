@@ -283,7 +283,8 @@ __global__ void k_colred_p2(const float* __restrict__ part, int n_chunks, int n_
 // ---- narrow-input layers (n_in <= NARROW_MAX, the networks' first layers: 1-8 inputs) ----
 // These are HBM-bound (K = n_in is tiny), so they are plain coalesced kernels, not GEMMs.
 constexpr int NARROW_MAX = 16;
-constexpr int NARROW_ROWS = 64;  // rows per CTA
+constexpr int NARROW_ROWS = 64;  // rows per CTA (forward)
+constexpr int NARROW_WROWS = 256;  // rows per CTA (weight gradient, pass 1)
 
 // forward Z = X W^T + b, A = act(Z): thread n owns output column n (weights in
 // registers), the CTA's NARROW_ROWS input rows are staged in shared memory, stores coalesced.
@@ -352,16 +353,18 @@ __global__ void __launch_bounds__(256) k_fwd_narrow(const float* __restrict__ X,
   }
 }
 
-// weight + bias gradient, pass 1: per chunk of NARROW_ROWS rows,
+// weight + bias gradient, pass 1: per chunk of wrows <= NARROW_WROWS rows (host: the long chunk when
+// it still gives >= 8 CTAs per SM - a quarter of the partials to write and re-read - else the
+// forward's 64; 16 loads of G in flight per thread),
 //   part[c][chunk][o][i] = sum_r G[r][o] X[r][i] (i < DIN), part[c][chunk][o][DIN] = sum_r G[r][o]
 template <int DIN>
 __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict__ G, int64_t sG, const float* __restrict__ X,
                                                          int64_t sX, int64_t rows, int n_out, float* __restrict__ part,
-                                                         int n_chunks, int sq) {
-  __shared__ __align__(16) float xs[NARROW_ROWS * DIN];
+                                                         int n_chunks, int sq, int wrows) {
+  __shared__ __align__(16) float xs[NARROW_WROWS * DIN];
   const int c = blockIdx.y, ch = blockIdx.x;
-  const int64_t r0 = (int64_t)ch * NARROW_ROWS;
-  const int nr = (int)min((int64_t)NARROW_ROWS, rows - r0);
+  const int64_t r0 = (int64_t)ch * wrows;
+  const int nr = (int)min((int64_t)wrows, rows - r0);
   const float* Xc = X + (int64_t)c * sX + r0 * DIN;
   for (int t = threadIdx.x; t < nr * DIN; t += blockDim.x) {
     const float xv = Xc[t];
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(256) k_wgrad_narrow_p1(const float* __restrict
 #pragma unroll
     for (int i = 0; i <= DIN; ++i) acc[i] = 0.f;
     const float* g = G + (int64_t)c * sG + r0 * n_out + o;
-#pragma unroll 8
-    for (int r = 0; r < nr; ++r) {  // (unrolled: 8 loads of G in flight per thread)
+#pragma unroll 16
+    for (int r = 0; r < nr; ++r) {  // (unrolled: 16 loads of G in flight per thread)
       float gv = g[(int64_t)r * n_out];
       if (sq) gv *= gv;
       float xr[DIN];
