@@ -516,3 +516,25 @@ def test_host_buffers_equal_device_buffers(name):
     np.testing.assert_array_equal(hd, d.cpu().numpy())
     np.testing.assert_array_equal(hT, T.cpu().numpy())
     np.testing.assert_array_equal(hG, G.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["mlp_ragged", "mlp_deep_narrow", "mlp_sin_nobias"])
+def test_grad_tiny_per_layer_engines(name):
+    """MLPs on the per-layer engines (hmc_debug_set_engine(2): no narrow engine), i.e. through the
+    one-pass output layer (k_out_fused; ragged 70 / 20-wide inputs, 333 / 64 rows: partial 256-row
+    chunks and 32-row blocks) - and, for the sin layer below the output, the four-kernel path."""
+    from paper_2507_14652_b200 import abi
+    arch, kw = TINY[name]
+    prob = make_tiny_problem(arch, n_chains=3, seed=TINY_SEED[name] + 100, noise=0.3, **kw)
+    th = jittered_states(prob, 3)
+    abi.hmc_debug_set_engine(2)
+    try:
+        with _ctx(prob) as c:
+            assert not abi.hmc_engine_info(c.ctx).startswith("narrow")
+            lp, g = gpu_grad(c, th)
+    finally:
+        abi.hmc_debug_set_engine(0)
+    t = ohmc.Target(prob)
+    for ci in range(3):
+        lr, gr = t.logp_grad(th[ci])
+        assert_grad_close(lp[ci], g[ci], lr, gr, f"{name} per-layer chain {ci}")
