@@ -1829,7 +1829,12 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         const int nk = (int)((rows + 31) / 32);
         if (pt < half_sms && nk >= 16) {  // fewest rounds of SM pairs per unit of K work
           double best = 1.0;
-          for (int ks = 2; ks <= std::min(16, nk / 8); ++ks) {
+          // overlapped weight gradients (wgrad_ov) run beside the input-gradient chain, which is the
+          // critical path: a split that fills every SM pair delays it, so they take at most half
+          // of the pairs (measured: cfg4 81.1k -> 85.2k evals/s, cfg3 +1 %)
+          int ks_cap = x->wgrad_ov ? std::max(1, half_sms / 2 / std::max(1, pt)) : 16;
+          if (const char* e = dev_env("HMC_KS_MAX")) ks_cap = atoi(e);
+          for (int ks = 2; ks <= std::min(ks_cap, nk / 8); ++ks) {
             const double cost = (double)((pt * ks + half_sms - 1) / half_sms) / ks;
             if (cost < best - 1e-12) { best = cost; L.ksplit = ks; }
           }
