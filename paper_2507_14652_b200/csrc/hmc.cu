@@ -876,6 +876,10 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     launch_gemm(x, a, true, true, st, "combine");
   }
   fork(1);
+  // the branch backward (the longer chain) continues on the combine's stream: its dB is launched
+  // programmatically behind the combine and gets its SMs before the trunk's dT does
+  static const bool swap_bt = !(dev_env("HMC_SWAP_BT") && atoi(dev_env("HMC_SWAP_BT")) == 0);
+  cudaStream_t s_br = (two && swap_bt) ? st : sb, s_tr = (two && swap_bt) ? sb : st;
   if (Nb.l_min >= 0) {  // dB = R T, times act' of the branch output layer
     GemmArgs a = gemm_base((int)x->n_c, p, (int)x->n_x, C);
     a.A = x->R; a.lda = x->n_x; a.sA = x->n_c * x->n_x;
@@ -883,7 +887,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.C = Nb.G[0]; a.ldc = p; a.sC = x->n_c * p;
     a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = (Bl.act == ACT_SIN) ? Bl.D : Bl.A; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
     if (Bl.bias_active && Nb.colsum) { a.colsum = Nb.colsum; a.s_colsum = (int64_t)((x->n_c + 31) / 32) * p; }
-    Nb.cs_ready = launch_gemm(x, a, true, false, sb, "dB") && a.colsum;
+    Nb.cs_ready = launch_gemm(x, a, true, false, s_br, "dB") && a.colsum;
   }
   if (Nt.l_min >= 0) {  // dT = R^T B, times act' of the trunk output layer
     GemmArgs a = gemm_base((int)x->n_x, p, (int)x->n_c, C);
@@ -892,10 +896,10 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
     a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
     if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
-    Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+    Nt.cs_ready = launch_gemm(x, a, false, false, s_tr, "dT") && a.colsum;
   }
-  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, sb);
-  if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, st);
+  if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, s_br);
+  if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, s_tr);
   join(1);
 }
 
@@ -1834,6 +1838,8 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
           // of the pairs (measured: cfg4 81.1k -> 85.2k evals/s, cfg3 +1 %)
           int ks_cap = x->wgrad_ov ? std::max(1, half_sms / 2 / std::max(1, pt)) : 16;
           if (const char* e = dev_env("HMC_KS_MAX")) ks_cap = atoi(e);
+          if (const char* e = dev_env("HMC_KS_LAST"))
+            if (L.l == x->nets[L.net].l_min) ks_cap = atoi(e);
           for (int ks = 2; ks <= std::min(ks_cap, nk / 8); ++ks) {
             const double cost = (double)((pt * ks + half_sms - 1) / half_sms) / ks;
             if (cost < best - 1e-12) { best = cost; L.ksplit = ks; }
