@@ -413,6 +413,9 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* tmem_holder = (uint32_t*)(bsplit + SB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // timeline (dev): kernel entry / prologue end / body end / exit of CTA 0 in the tail of row 0
+  const bool tl_k = mn.prof >= 2 && mn.prof - 2 == mn.vid && blockIdx.x == 0 && threadIdx.x == 0;
+  if (tl_k) g_tctl[0][TL_N - 1] = clock64();
   const int n_mt = (a.M + BM - 1) / BM, n_nt = (a.N + BN - 1) / BN;
   const int tiles_per_b = n_mt * n_nt;
   // CTA pairs (cluster of 2): the pair covers M tiles 2p and 2p+1 of the same (batch, N tile)
@@ -482,6 +485,7 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t tmem_base = *tmem_holder;
   unsigned long long pacc[3] = {0ull, 0ull, 0ull};
   const unsigned long long t_k0 = mn.prof ? clock64() : 0ull;
+  if (tl_k) g_tctl[0][TL_N - 2] = t_k0;
 
   if (warp == W_TMA_A) {
     // ============================ TMA producer: A ring ============================
@@ -1158,9 +1162,11 @@ __global__ void __launch_bounds__(NT, 1)
     }
     if (warp == W_TMA_A) atomicAdd(&g_tcprof[mn.vid][P_TOTAL], clock64() - t_k0);
   }
+  if (tl_k) g_tctl[0][TL_N - 3] = clock64();
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // no CTA leaves while its peer may still multicast into it or arrive on it
+  if (tl_k) g_tctl[0][TL_N - 4] = clock64();
   if (warp == W_MMA) tmem_dealloc2(tmem_base, 512);
 }
 
