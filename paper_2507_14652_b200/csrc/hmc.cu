@@ -144,6 +144,10 @@ struct hmc_ctx {
   // DeepONet (aligned, ROWS): branch and trunk enqueued on two streams inside the graph
   bool two_streams = false;
   bool wgrad_ov = false;  // weight gradients on their own stream per net (any layout but xb / unaligned)
+  // K split of the DeepONet dT = R^T B GEMM (dt_ksplit): ks row slabs as extra batch entries, partial
+  // products [C x ks x n_x x p] summed in slab order by k_dact_ksplit_reduce
+  int dt_ks = 1;
+  float* dt_part = nullptr;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   float* d_inv_mass = nullptr;
@@ -620,6 +624,48 @@ void xb_combine(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr) {
   launch_gemm(x, a, true, true, st, "combine");
 }
 
+// K split of dT = R^T B (M = n_x, N = p, K = n_c per chain).  With few query points and many
+// conditions (cfg4: 100 x 100 outputs from 1000 rows, 16 chains) the GEMM is one tile per chain
+// whose K blocks run serially on 16 of the 74 SM pairs - the longest kernel of the trunk's
+// backward chain.  The largest ks <= 8 that divides K, keeps every slab >= 4 K blocks with aligned
+// strides and fits all pair tiles x ks in one round of SM pairs; 1 = no split.
+int dt_ksplit(const hmc_ctx* x, int M, int N, int K, int batch) {
+  if (!x->tc.enabled) return 1;
+  GemmArgs a = gemm_base(M, N, K, batch);
+  const int half_sms = std::max(1, x->tc.num_sms / 2);
+  const int pt = TcPlanner::pair_tiles(a);
+  for (int ks = 8; ks >= 2; --ks) {
+    if (K % ks || K / ks < 128 || (int64_t)pt * ks > half_sms) continue;
+    if (((int64_t)(K / ks) * M) % 4 || ((int64_t)(K / ks) * N) % 4) continue;
+    return ks;
+  }
+  return 1;
+}
+
+// dT with the context's K split when the launch is the one it was planned for (operands whose
+// chain stride is exactly their K rows); returns whether the bias-gradient column partials of the
+// result are in a.colsum (only the unsplit GEMM's epilogue writes them)
+bool launch_dT(hmc_ctx* x, const GemmArgs& a, cudaStream_t st) {
+  const int ks = x->dt_ks;
+  if (ks > 1 && x->dt_part && a.K % ks == 0 && a.sA == (int64_t)a.K * a.lda && a.sB == (int64_t)a.K * a.ldb &&
+      a.ldc == a.N && a.sC == (int64_t)a.M * a.N && a.ld_dsrc == a.N && a.s_dsrc == a.sC &&
+      a.M == (int)x->n_x && a.K == (int)x->n_c && a.batch == x->C && ks == dt_ksplit(x, a.M, a.N, a.K, a.batch)) {
+    GemmArgs b = gemm_base(a.M, a.N, a.K / ks, a.batch * ks);
+    b.A = a.A; b.lda = a.lda; b.sA = (int64_t)b.K * a.lda;
+    b.B = a.B; b.ldb = a.ldb; b.sB = (int64_t)b.K * a.ldb;
+    b.C = x->dt_part; b.ldc = a.N; b.sC = a.sC;
+    if (x->tc.accepts(b, false, false)) {
+      launch_gemm(x, b, false, false, st, "dT");
+      const int64_t MN = (int64_t)a.M * a.N;
+      k_dact_ksplit_reduce<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((MN + 255) / 256, 64)), a.batch), 256, 0, st>>>(
+          x->dt_part, ks, MN, a.act, a.dsrc, a.dsrc, a.C);
+      x->launches++;
+      return false;
+    }
+  }
+  return launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+}
+
 void xb_dB(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr, float* out = nullptr) {
   const LayerInfo& Bl = x->layers[x->nets[0].layers.back()];
   const LayerInfo& Tl = x->layers[x->nets[1].layers.back()];
@@ -648,7 +694,7 @@ void xb_dT(hmc_ctx* x, cudaStream_t st, const float* Ball = nullptr) {
   a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
   a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
   if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
-  Nt.cs_ready = launch_gemm(x, a, false, false, st, "dT") && a.colsum;
+  Nt.cs_ready = launch_dT(x, a, st);
 }
 
 // (single-stream sequences, used by the emulated-exchange phases hmc_debug_data_phase)
@@ -896,7 +942,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.C = Nt.G[0]; a.ldc = p; a.sC = x->n_x * p;
     a.epi = EPI_DACT; a.act = Tl.act; a.dsrc = (Tl.act == ACT_SIN) ? Tl.D : Tl.A; a.ld_dsrc = p; a.s_dsrc = x->n_x * p;
     if (Tl.bias_active && Nt.colsum) { a.colsum = Nt.colsum; a.s_colsum = (int64_t)((x->n_x + 31) / 32) * p; }
-    Nt.cs_ready = launch_gemm(x, a, false, false, s_tr, "dT") && a.colsum;
+    Nt.cs_ready = launch_dT(x, a, s_tr);
   }
   if (Nb.l_min >= 0) enqueue_backward_net(x, Nb, (int)Nb.layers.size() - 1, 0, s_br);
   if (Nt.l_min >= 0) enqueue_backward_net(x, Nt, (int)Nt.layers.size() - 1, 0, s_tr);
@@ -2034,6 +2080,12 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
       }
     }
   }
+  if (x->kind == HMC_DEEPONET && !x->unaligned && x->nets[1].l_min >= 0) {
+    const int p = x->layers[x->nets[1].layers.back()].n_out;
+    x->dt_ks = dt_ksplit(x, (int)x->n_x, p, (int)x->n_c, C);
+    if (const char* e = dev_env("HMC_DT_KS")) { if (atoi(e) <= 1) x->dt_ks = 1; }  // dev A/B: 1 = no split
+    if (x->dt_ks > 1) x->dt_part = dalloc<float>(x, (size_t)C * x->dt_ks * x->n_x * p, err);
+  }
   plan_masked_wgrad(x, slot, err);
   CK(cudaMallocHost((void**)&x->h_rec, sizeof(Rec)));
   CK(cudaMallocHost((void**)&x->h_eps, sizeof(double)));
@@ -2073,6 +2125,7 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
     for (auto& L : x->layers) { nm += L.mwg; na += L.any_active && !is_narrow(L); }
     if (nm) x->engine += " + masked wgrad (" + std::to_string(nm) + " of " + std::to_string(na) + " layers)";
   }
+  if (x->dt_ks > 1) x->engine += " + dT K split " + std::to_string(x->dt_ks);
   CK(cudaDeviceSynchronize());
 }
 

@@ -851,6 +851,20 @@ __device__ __forceinline__ float dact_at(int act, const float* __restrict__ A, c
   return 1.f;
 }
 
+// ---- K-split dT (DeepONet trunk output gradient): G[c][t] = (sum_s part[c * ks + s][t]) act'(t),
+//      the ks row slabs' partial products summed in slab order; t over the M x N tile of chain c ----
+__global__ void k_dact_ksplit_reduce(const float* __restrict__ part, int ks, int64_t MN, int act,
+                                     const float* __restrict__ A, const float* __restrict__ D,
+                                     float* __restrict__ G) {
+  const int64_t c = blockIdx.y;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < MN; t += (int64_t)gridDim.x * blockDim.x) {
+    const float* p = part + c * ks * MN + t;
+    float acc = 0.f;
+    for (int s = 0; s < ks; ++s) acc += p[(int64_t)s * MN];
+    G[c * MN + t] = acc * dact_at(act, A, D, c * MN + t);
+  }
+}
+
 // combine + residual: block (c, chain), one warp per pair row x (lanes over k).  V != nullptr:
 // R_cx = (V_cx - F_cx) / sigma^2 and the fixed-order fp64 partials sum r^2, sum R of the block go
 // to slot c of the chain; V == nullptr (prediction): R_cx = F_cx.

@@ -57,6 +57,10 @@ TINY = {
     "deeponet_ragged": (ArchSpec("deeponet", (NetSpec.plain((7, 130, 64, 50)),
                                               NetSpec.plain((3, 70, 50), last="tanh")), has_b0=True),
                         dict(n_c=150, n_x=201, active_frac=0.5)),
+    # few query points, many conditions: the dT = R^T B GEMM splits K into 2 row slabs (dt_ksplit)
+    "deeponet_dt_ksplit": (ArchSpec("deeponet", (NetSpec.plain((7, 64, 40)),
+                                                 NetSpec.plain((3, 70, 40), last="tanh")), has_b0=True),
+                           dict(n_c=300, n_x=70, active_frac=0.5)),
     "deeponet_sin": (ArchSpec("deeponet", (NetSpec((4, 20, 12), ("sin", "identity"), (True, True)),
                                            NetSpec((2, 16, 12), ("tanh", "sin"), (True, False))),
                               has_b0=False), dict(n_c=33, n_x=65, active_frac=0.9)),
@@ -65,7 +69,7 @@ TINY = {
 
 # fixed per-case seeds (reproducible across processes, unlike salted str hashes)
 TINY_SEED = {"mlp_ragged": 21, "mlp_sin_nobias": 22, "mlp_deep_narrow": 23, "deeponet_ragged": 24,
-             "deeponet_sin": 25}
+             "deeponet_sin": 25, "deeponet_dt_ksplit": 26}
 
 
 @pytest.mark.parametrize("name", sorted(TINY))
@@ -74,6 +78,9 @@ def test_grad_tiny(name):
     prob = make_tiny_problem(arch, n_chains=3, seed=TINY_SEED[name], noise=0.3, **kw)
     th = jittered_states(prob, 3)
     with _ctx(prob) as c:
+        if name == "deeponet_dt_ksplit":
+            from paper_2507_14652_b200 import abi
+            assert "dT K split 2" in abi.hmc_engine_info(c.ctx), abi.hmc_engine_info(c.ctx)
         lp, g = gpu_grad(c, th)
     t = ohmc.Target(prob)
     for ci in range(3):
