@@ -26,6 +26,7 @@ struct GemmArgs {
   float* C; int64_t ldc, sC;
   int ones_col;  // >= 0: B(k, n == ones_col) = 1 (bias column of the weight gradient)
   int epi;
+  int max_pairs;  // tcgen05 engine: > 0 caps the launch's CTA pairs (several tiles per pair); 0 = one round of the SMs
   int act;       // EPI_FWD: activation of this layer; EPI_DACT: activation of the producer
   // EPI_FWD
   const float* bias; int64_t s_bias;  // per-batch stride (nullptr = no bias)

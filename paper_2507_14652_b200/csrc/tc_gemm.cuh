@@ -1400,7 +1400,14 @@ struct TcPlanner {
     if (!ok) return cudaErrorInvalidValue;
     const int pairs = (((a.M + tc::BM - 1) / tc::BM + 1) / 2) * ((a.N + BN - 1) / BN) * a.batch *
                       ((a.epi == EPI_WGRAD && a.ksplit > 1) ? a.ksplit : 1);
-    const int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
+    int pair_cap = num_sms / 2;
+    if (a.max_pairs > 0 && a.max_pairs < pair_cap) pair_cap = a.max_pairs;
+    // dev A/B: fewer, longer-lived CTA pairs (several tiles each) for the launches of one EPI class
+    // (HMC_TC_GRIDCAP = pairs, HMC_TC_GRIDCAP_EPI = bit mask of EPI ids, default all)
+    static const int gridcap = dev_env("HMC_TC_GRIDCAP") ? atoi(dev_env("HMC_TC_GRIDCAP")) : 0;
+    static const int gridcap_epi = dev_env("HMC_TC_GRIDCAP_EPI") ? atoi(dev_env("HMC_TC_GRIDCAP_EPI")) : 0xff;
+    if (gridcap > 0 && ((gridcap_epi >> a.epi) & 1) && gridcap < pair_cap) pair_cap = gridcap;
+    const int grid = 2 * (pairs < pair_cap ? pairs : pair_cap);
     int nv = 0;
     tc::MnDesc md = mn;
     md.vid = (int)(v - tc_variants<BN>(&nv));
