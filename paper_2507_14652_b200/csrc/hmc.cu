@@ -942,6 +942,7 @@ void enqueue_body(hmc_ctx* x, cudaStream_t st) {
     a.C = Nb.G[0]; a.ldc = p; a.sC = x->n_c * p;
     a.epi = EPI_DACT; a.act = Bl.act; a.dsrc = (Bl.act == ACT_SIN) ? Bl.D : Bl.A; a.ld_dsrc = p; a.s_dsrc = x->n_c * p;
     if (Bl.bias_active && Nb.colsum) { a.colsum = Nb.colsum; a.s_colsum = (int64_t)((x->n_c + 31) / 32) * p; }
+    if (const char* e = dev_env("HMC_DB_HALVE")) { if (atoi(e) == 0) a.max_pairs = 1 << 20; }  // dev A/B: dB keeps its full grid
     Nb.cs_ready = launch_gemm(x, a, true, false, s_br, "dB") && a.colsum;
   }
   if (Nt.l_min >= 0) {  // dT = R^T B, times act' of the trunk output layer
