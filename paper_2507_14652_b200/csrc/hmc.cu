@@ -1890,9 +1890,10 @@ void setup_impl(hmc_ctx* x, const hmc_arch* arch, const hmc_data* data, const hm
         if (pt < half_sms && nk >= 16) {  // fewest rounds of SM pairs per unit of K work
           double best = 1.0;
           // overlapped weight gradients (wgrad_ov) run beside the input-gradient chain, which is the
-          // critical path: a split that fills every SM pair delays it, so they take at most half
-          // of the pairs (measured: cfg4 81.1k -> 85.2k evals/s, cfg3 +1 %)
-          int ks_cap = x->wgrad_ov ? std::max(1, half_sms / 2 / std::max(1, pt)) : 16;
+          // critical path: a split that fills every SM pair delays it, so they take at most a
+          // quarter of the pairs (measured: half of the pairs cfg4 81.1k -> 85.2k evals/s, cfg3 +1 %;
+          // a quarter, beside the halved input-gradient grids, cfg4 90.6k -> 92.9k)
+          int ks_cap = x->wgrad_ov ? std::max(1, half_sms / 4 / std::max(1, pt)) : 16;
           if (const char* e = dev_env("HMC_KS_MAX")) ks_cap = atoi(e);
           if (const char* e = dev_env("HMC_KS_LAST"))
             if (L.l == x->nets[L.net].l_min) ks_cap = atoi(e);
